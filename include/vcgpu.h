@@ -1,0 +1,167 @@
+/* include/vcgpu.h — the C-ABI of the B200-native vertex-cover search engine (libvcgpu.so).
+ *
+ * Plain pointers and sizes only. Every entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj). All functions return an int status code
+ * (VCG_OK = 0); on failure vcg_last_error() holds a thread-local message whose text follows the
+ * reference's exception text where one exists (e.g. ParseError "line N: ...", graph.hpp:17-26).
+ *
+ * Ownership: the caller owns every buffer it passes in (never retained beyond the call, except
+ * that vcg_graph_* copy their inputs). The library owns vcg_graph objects (free with
+ * vcg_graph_destroy) and the arrays inside a vcg_result (free with vcg_result_free). Device
+ * copies of a graph are created lazily by the first solve on a device and live until
+ * vcg_graph_destroy.
+ */
+#ifndef VCGPU_H
+#define VCGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VCG_API __attribute__((visibility("default")))
+
+/* status codes */
+enum {
+    VCG_OK = 0,
+    VCG_EINVAL = 1,   /* std::invalid_argument in the reference (scheduler.cpp:20-29,330) */
+    VCG_EPARSE = 2,   /* vcsolve::ParseError (graph.hpp:17-26) */
+    VCG_ECUDA = 3,    /* CUDA/device error: no reference counterpart (CPU-only reference) */
+    VCG_ENOMEM = 4,
+    VCG_ERANGE = 5    /* brute_force_mvc limit (solver_seq.cpp:174-175) */
+};
+
+typedef struct vcg_graph vcg_graph; /* opaque: BaseGraph (graph.hpp:34-53) + device copies */
+
+/* ------------------------------------------------------------------ graph (host side) */
+
+/* BaseGraph from an already-built CSR (offsets u64[n+1], neighbors u32[2m], sorted,
+ * duplicate-free, symmetric). Validated; replaces constructing BaseGraph directly. */
+VCG_API int vcg_graph_from_csr(uint32_t n, uint64_t m, const uint64_t* offsets,
+                               const uint32_t* neighbors, uint32_t id_base, vcg_graph** out);
+/* make_graph (graph.hpp:57-59, graph.cpp:22-54): pairs = 2*num_pairs ids in [0, n). */
+VCG_API int vcg_make_graph(uint32_t n, uint64_t num_pairs, const uint32_t* pairs,
+                           uint32_t id_base, vcg_graph** out);
+/* parse_edge_list (graph.hpp:64, graph.cpp:81-114) and parse_dimacs (graph.hpp:68,
+ * graph.cpp:116-159) over an in-memory text of `len` bytes. VCG_EPARSE on malformed input. */
+VCG_API int vcg_parse_edge_list(const char* text, size_t len, vcg_graph** out);
+VCG_API int vcg_parse_dimacs(const char* text, size_t len, vcg_graph** out);
+/* complement (graph.hpp:71, graph.cpp:161-185) */
+VCG_API int vcg_complement(const vcg_graph* g, vcg_graph** out);
+/* write_edge_list (graph.hpp:74, graph.cpp:187-193): *text is library-owned until
+ * vcg_free_buffer. */
+VCG_API int vcg_write_edge_list(const vcg_graph* g, char** text, size_t* len);
+VCG_API void vcg_free_buffer(void* p);
+VCG_API void vcg_graph_destroy(vcg_graph* g);
+
+VCG_API uint32_t vcg_graph_num_vertices(const vcg_graph* g);
+VCG_API uint64_t vcg_graph_num_edges(const vcg_graph* g);
+VCG_API uint32_t vcg_graph_id_base(const vcg_graph* g);
+/* Borrowed views of the CSR (valid until vcg_graph_destroy). */
+VCG_API const uint64_t* vcg_graph_offsets(const vcg_graph* g);
+VCG_API const uint32_t* vcg_graph_neighbors(const vcg_graph* g);
+/* BaseGraph::has_edge (graph.cpp:14-20); BaseGraph::operator== (graph.hpp:52) */
+VCG_API int vcg_has_edge(const vcg_graph* g, uint32_t u, uint32_t v);
+VCG_API int vcg_graph_equal(const vcg_graph* a, const vcg_graph* b);
+/* check_graph_invariants (graph.cpp:195-211) */
+VCG_API int vcg_check_invariants(const vcg_graph* g);
+
+/* greedy_approx (bounds.hpp:28-32, bounds.cpp:7-19): same cover as the reference.
+ * cover needs n slots, receives internal ids ascending. */
+VCG_API int vcg_greedy(const vcg_graph* g, uint32_t* size, uint32_t* cover);
+/* brute_force_mvc (solver_seq.hpp:50-52, solver_seq.cpp:173-211): VCG_ERANGE when n > 20.
+ * cover receives ORIGINAL ids (internal + id_base), like the reference. */
+VCG_API int vcg_brute_force(const vcg_graph* g, uint32_t* size, uint32_t* cover);
+/* verify_cover (bounds.hpp:44, bounds.cpp:32-45) over internal ids. */
+VCG_API int vcg_verify_cover(const vcg_graph* g, const uint32_t* cover, uint32_t len, int* ok);
+
+/* ------------------------------------------------------------------------------ solve */
+
+enum { VCG_MVC = 0, VCG_PVC = 1 };                         /* SolveMode (bounds.hpp:13-22) */
+enum { VCG_HYBRID = 0, VCG_SEQ = 1, VCG_STACKONLY = 2 };   /* bindings.cpp:75-93 strategies */
+enum { VCG_COMPLETE = 0, VCG_TIMEOUT = 1, VCG_BUDGET = 2 }; /* RunStatus (solver_seq.hpp:22) */
+enum { VCG_RULES_REFERENCE = 0, VCG_RULES_PARALLEL = 1 };
+
+/* SchedulerConfig (scheduler.hpp:17-25) + SolveLimits (solver_seq.hpp:28-31) + GPU knobs.
+ * Initialise with vcg_params_init (reference defaults: capacity 4096, fraction 0.5, depth 8,
+ * backoff 50 us, bindings.cpp:174-202). */
+typedef struct {
+    int32_t mode;               /* VCG_MVC | VCG_PVC */
+    uint32_t k;                 /* PVC parameter, >= 1 */
+    int32_t strategy;           /* VCG_HYBRID | VCG_SEQ | VCG_STACKONLY */
+    uint32_t workers;           /* worker count (one worker = one warp or one block);
+                                   0 = fill every SM of the device */
+    uint64_t capacity;          /* worklist capacity (entries) */
+    double threshold_fraction;  /* (0, 1] → threshold = clamp(llround(f*cap), 1, cap) */
+    uint32_t depth;             /* StackOnly sub-tree depth in [1, 30] */
+    uint64_t backoff_us;        /* idle back-off (maps to __nanosleep) */
+    double timeout_s;           /* < 0: none */
+    uint64_t node_budget;       /* 0: none */
+    int32_t device;             /* CUDA device ordinal */
+    int32_t rules;              /* VCG_RULES_REFERENCE (bit-exact reference node order) or
+                                   VCG_RULES_PARALLEL (block-parallel rule rounds) */
+    uint32_t block_warps;       /* warps per CTA, 0 = auto */
+    int32_t engine;             /* 0 auto, 1 dense (n <= 1024, warp per node),
+                                   2 sparse (any n, CTA per node) */
+    int32_t instrument;         /* 1: per-worker phase cycle counters */
+    uint32_t initial_best;      /* MVC: external upper bound (e.g. from another rank),
+                                   0 = none; never replaces the greedy certificate */
+    /* Seeding (multi-GPU frontier shares): when num_seeds > 0, the worklist starts with these
+       nodes instead of the root. seeds = num_seeds records of
+       [cover_count u32, edge_count u32, degrees u32[n]] (kRemoved = 0xFFFFFFFF). */
+    uint64_t num_seeds;
+    const uint32_t* seeds;
+    /* Mailbox (pinned host memory, written by the host, polled by the device ~every 50 us):
+       mailbox[0] = external best bound (MVC, 0 = none), mailbox[1] = cancel request.
+       Null = none. */
+    volatile uint32_t* mailbox;
+} vcg_params;
+
+typedef struct {
+    int32_t status;             /* VCG_COMPLETE | VCG_TIMEOUT | VCG_BUDGET */
+    uint32_t size;              /* Solution.size (0 for infeasible PVC) */
+    int32_t feasible;
+    uint32_t greedy_size;       /* ParallelRun.greedy_size */
+    uint32_t cover_len;
+    uint32_t* cover;            /* ORIGINAL ids (internal + id_base), ascending */
+    int32_t cover_from_search;  /* 0: the greedy certificate was the answer */
+    uint32_t num_workers;
+    uint64_t* worker_nodes;     /* WorkerMetrics.nodes_visited, per worker */
+    uint64_t* worker_stack_high_water;
+    uint64_t nodes_total;
+    uint64_t wl_added, wl_removed, wl_max_size, wl_current_size; /* GlobalWorklist::Stats */
+    double wall_ms;             /* ParallelRun.wall_ms: greedy + setup + search + readback */
+    double device_ms;           /* search kernel(s), CUDA events */
+    double greedy_ms;
+    double h2d_ms;
+    uint64_t h2d_bytes, d2h_bytes;
+    /* roofline counters: rule rounds, max-degree passes, children built */
+    uint64_t rounds, maxdeg_passes, children, removals;
+    uint32_t degree_bytes;      /* w: bytes per degree entry in the engine's node layout */
+    uint32_t n_padded;          /* n rounded to the engine's lane layout */
+    int32_t engine;             /* engine that ran: 1 dense, 2 sparse */
+    uint32_t grid_blocks, block_threads;
+    uint64_t phase_cycles[10];  /* Phase order of metrics.hpp:15-26, summed over workers */
+    uint64_t active_cycles;     /* summed over workers */
+} vcg_result;
+
+VCG_API void vcg_params_init(vcg_params* p);
+/* run_hybrid / run_stackonly (scheduler.hpp:48,55) and solve_mvc_seq / solve_pvc_seq
+ * (solver_seq.hpp:43-48) on the GPU: greedy seed (host), CSR upload, one persistent kernel,
+ * result readback. Blocking. */
+VCG_API int vcg_solve(const vcg_graph* g, const vcg_params* p, vcg_result* out);
+VCG_API void vcg_result_free(vcg_result* r);
+
+/* Number of CUDA devices visible (0 when no driver / no GPU). */
+VCG_API int vcg_device_count(void);
+/* Thread-local text of the last error. */
+VCG_API const char* vcg_last_error(void);
+/* Library version string. */
+VCG_API const char* vcg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VCGPU_H */

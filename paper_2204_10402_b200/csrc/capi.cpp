@@ -1,0 +1,312 @@
+// capi.cpp — the extern "C" boundary (include/vcgpu.h). Maps C++ exceptions to status codes
+// the way the reference's pybind11 layer maps them to Python (bindings.cpp:106 ParseError ->
+// ValueError, std::invalid_argument -> ValueError) and runs the host part of run_hybrid
+// (scheduler.cpp:328-359): validate, greedy seed, device search, certificate assembly.
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/vcgpu.h"
+#include "engine.hpp"
+#include "host_graph.hpp"
+
+struct vcg_graph {
+    vcg::Graph g;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const vcg::ParseError& e) {
+        return fail(VCG_EPARSE, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(VCG_EINVAL, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(VCG_ENOMEM, "out of memory");
+    } catch (const std::runtime_error& e) {
+        const std::string w = e.what();
+        return fail(w.rfind("CUDA", 0) == 0 ? VCG_ECUDA : VCG_EINVAL, w);
+    } catch (...) {
+        return fail(VCG_EINVAL, "unknown error");
+    }
+}
+
+int emit(vcg::Graph&& g, vcg_graph** out) {
+    if (!out) return fail(VCG_EINVAL, "null output handle");
+    *out = new vcg_graph{std::move(g)};
+    return VCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vcg_last_error(void) { return g_err.c_str(); }
+const char* vcg_version(void) { return "vcgpu 0.1.0 (sm_100a)"; }
+int vcg_device_count(void) { return vcg::device_count(); }
+
+int vcg_graph_from_csr(uint32_t n, uint64_t m, const uint64_t* offsets,
+                       const uint32_t* neighbors, uint32_t id_base, vcg_graph** out) {
+    return guarded([&]() -> int {
+        if (!offsets || (m && !neighbors)) return fail(VCG_EINVAL, "null CSR array");
+        vcg::Graph g;
+        g.n = n;
+        g.m = m;
+        g.id_base = id_base;
+        g.off.assign(offsets, offsets + size_t(n) + 1);
+        g.nbr.assign(neighbors, neighbors + 2 * m);
+        if (!vcg::check_invariants(g)) return fail(VCG_EINVAL, "CSR violates graph invariants");
+        return emit(std::move(g), out);
+    });
+}
+
+int vcg_make_graph(uint32_t n, uint64_t num_pairs, const uint32_t* pairs, uint32_t id_base,
+                   vcg_graph** out) {
+    return guarded([&]() -> int {
+        if (num_pairs && !pairs) return fail(VCG_EINVAL, "null pairs");
+        std::vector<std::pair<uint32_t, uint32_t>> e(num_pairs);
+        for (uint64_t i = 0; i < num_pairs; ++i) e[i] = {pairs[2 * i], pairs[2 * i + 1]};
+        return emit(vcg::make_graph(n, e, id_base), out);
+    });
+}
+
+int vcg_parse_edge_list(const char* text, size_t len, vcg_graph** out) {
+    return guarded([&]() -> int { return emit(vcg::parse_edge_list(text ? text : "", text ? len : 0), out); });
+}
+
+int vcg_parse_dimacs(const char* text, size_t len, vcg_graph** out) {
+    return guarded([&]() -> int { return emit(vcg::parse_dimacs(text ? text : "", text ? len : 0), out); });
+}
+
+int vcg_complement(const vcg_graph* g, vcg_graph** out) {
+    return guarded([&]() -> int {
+        if (!g) return fail(VCG_EINVAL, "null graph");
+        return emit(vcg::complement(g->g), out);
+    });
+}
+
+int vcg_write_edge_list(const vcg_graph* g, char** text, size_t* len) {
+    return guarded([&]() -> int {
+        if (!g || !text || !len) return fail(VCG_EINVAL, "null argument");
+        std::string s = vcg::write_edge_list(g->g);
+        char* p = static_cast<char*>(std::malloc(s.size() + 1));
+        if (!p) return fail(VCG_ENOMEM, "out of memory");
+        std::memcpy(p, s.data(), s.size());
+        p[s.size()] = 0;
+        *text = p;
+        *len = s.size();
+        return VCG_OK;
+    });
+}
+
+void vcg_free_buffer(void* p) { std::free(p); }
+void vcg_graph_destroy(vcg_graph* g) { delete g; }
+uint32_t vcg_graph_num_vertices(const vcg_graph* g) { return g ? g->g.n : 0; }
+uint64_t vcg_graph_num_edges(const vcg_graph* g) { return g ? g->g.m : 0; }
+uint32_t vcg_graph_id_base(const vcg_graph* g) { return g ? g->g.id_base : 0; }
+const uint64_t* vcg_graph_offsets(const vcg_graph* g) { return g ? g->g.off.data() : nullptr; }
+const uint32_t* vcg_graph_neighbors(const vcg_graph* g) { return g ? g->g.nbr.data() : nullptr; }
+
+int vcg_has_edge(const vcg_graph* g, uint32_t u, uint32_t v) {
+    if (!g || u >= g->g.n || v >= g->g.n) return 0;
+    return g->g.has_edge(u, v) ? 1 : 0;
+}
+
+int vcg_graph_equal(const vcg_graph* a, const vcg_graph* b) {
+    if (!a || !b) return 0;
+    const vcg::Graph &x = a->g, &y = b->g;
+    return x.n == y.n && x.m == y.m && x.id_base == y.id_base && x.off == y.off && x.nbr == y.nbr;
+}
+
+int vcg_check_invariants(const vcg_graph* g) { return g && vcg::check_invariants(g->g) ? 1 : 0; }
+
+int vcg_greedy(const vcg_graph* g, uint32_t* size, uint32_t* cover) {
+    return guarded([&]() -> int {
+        if (!g || !size) return fail(VCG_EINVAL, "null argument");
+        vcg::Greedy r = vcg::greedy_approx(g->g);
+        *size = r.size;
+        if (cover) std::memcpy(cover, r.cover.data(), r.cover.size() * 4);
+        return VCG_OK;
+    });
+}
+
+int vcg_brute_force(const vcg_graph* g, uint32_t* size, uint32_t* cover) {
+    return guarded([&]() -> int {
+        if (!g || !size) return fail(VCG_EINVAL, "null argument");
+        if (g->g.n > 20) return fail(VCG_ERANGE, "brute force oracle is limited to 20 vertices");
+        std::vector<uint32_t> c;
+        *size = vcg::brute_force(g->g, c);
+        if (cover)
+            for (size_t i = 0; i < c.size(); ++i) cover[i] = c[i] + g->g.id_base;
+        return VCG_OK;
+    });
+}
+
+int vcg_verify_cover(const vcg_graph* g, const uint32_t* cover, uint32_t len, int* ok) {
+    return guarded([&]() -> int {
+        if (!g || !ok || (len && !cover)) return fail(VCG_EINVAL, "null argument");
+        *ok = vcg::verify_cover(g->g, cover, len) ? 1 : 0;
+        return VCG_OK;
+    });
+}
+
+void vcg_params_init(vcg_params* p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->mode = VCG_MVC;
+    p->strategy = VCG_HYBRID;
+    p->capacity = 4096;             // bindings.cpp:177
+    p->threshold_fraction = 0.5;    // bindings.cpp:177
+    p->depth = 8;                   // bindings.cpp:177
+    p->backoff_us = 50;             // bindings.cpp:178
+    p->timeout_s = -1.0;
+    p->rules = VCG_RULES_REFERENCE;
+}
+
+int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
+    return guarded([&]() -> int {
+        if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
+        std::memset(out, 0, sizeof(*out));
+        const vcg::Graph& g = gh->g;
+        // validate_config (scheduler.cpp:20-29) + the k >= 1 check (:330)
+        if (p->capacity < 1) return fail(VCG_EINVAL, "worklist_capacity must be >= 1");
+        if (!(p->threshold_fraction > 0.0) || p->threshold_fraction > 1.0)
+            return fail(VCG_EINVAL, "threshold_fraction must be in (0, 1]");
+        if (p->depth < 1 || p->depth > 30)
+            return fail(VCG_EINVAL, "stackonly_depth must be in [1, 30]");
+        if (p->mode == VCG_PVC && p->k < 1) return fail(VCG_EINVAL, "pvc requires k >= 1");
+        if (p->strategy < VCG_HYBRID || p->strategy > VCG_STACKONLY)
+            return fail(VCG_EINVAL, "unknown strategy");
+        if (p->strategy == VCG_STACKONLY)
+            return fail(VCG_EINVAL, "the stackonly strategy is not available in this build");
+        if (p->num_seeds && !p->seeds) return fail(VCG_EINVAL, "null seeds");
+        const auto t0 = std::chrono::steady_clock::now();
+        const bool pvc = p->mode == VCG_PVC;
+
+        // greedy seed (scheduler.cpp:333-340), counted in wall_ms like the reference
+        vcg::Greedy greedy = vcg::greedy_approx(g);
+        const auto t1 = std::chrono::steady_clock::now();
+        out->greedy_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        out->greedy_size = greedy.size;
+
+        vcg::SolveSpec s;
+        s.pvc = pvc;
+        s.k = p->k;
+        s.strategy = p->strategy;
+        s.workers = p->workers;
+        s.capacity = p->capacity;
+        // worklist_threshold (scheduler.cpp:14-18)
+        long long t = std::llround(p->threshold_fraction * double(p->capacity));
+        s.threshold = (uint64_t)std::max<long long>(1, std::min<long long>(t, (long long)p->capacity));
+        s.depth = p->depth;
+        s.backoff_us = p->backoff_us;
+        s.timeout_s = p->timeout_s;
+        s.node_budget = p->node_budget;
+        s.device = p->device;
+        s.rules = p->rules;
+        s.block_warps = p->block_warps;
+        s.engine = p->engine;
+        s.instrument = p->instrument != 0;
+        s.best = pvc ? p->k : greedy.size;
+        if (!pvc && p->initial_best && p->initial_best < s.best) s.best = p->initial_best;
+        // stack_bound_for (scheduler.cpp:118-121)
+        s.stack_bound = pvc ? std::min<uint32_t>(p->k, g.n) : greedy.size;
+        s.seeds = p->seeds;
+        s.num_seeds = p->num_seeds;
+        s.mailbox = p->mailbox;
+
+        vcg::SolveOut r;
+        if (g.n == 0) {
+            // no vertex: one root visit, nothing to branch on (MVC 0; PVC feasible, empty)
+            r.worker_nodes.assign(1, 1);
+            r.worker_high_water.assign(1, 0);
+            r.found = pvc;
+            r.wl_added = r.wl_removed = 1;
+        } else {
+            vcg::solve_on_device(g, s, r);
+        }
+
+        // finish_run (scheduler.cpp:299-324): certificate in original ids
+        const std::vector<uint32_t>* cov = nullptr;
+        if (pvc) {
+            out->feasible = r.found ? 1 : 0;
+            if (r.found) {
+                cov = &r.cover;
+                out->size = (uint32_t)r.cover.size();
+                out->cover_from_search = 1;
+            }
+        } else {
+            out->feasible = 1;
+            if (r.found && r.cover.size() < greedy.size) {
+                cov = &r.cover;
+                out->cover_from_search = 1;
+            } else {
+                cov = &greedy.cover;
+            }
+            out->size = (uint32_t)cov->size();
+        }
+        if (cov && !cov->empty()) {
+            out->cover = static_cast<uint32_t*>(std::malloc(cov->size() * 4));
+            for (size_t i = 0; i < cov->size(); ++i) out->cover[i] = (*cov)[i] + g.id_base;
+        }
+        out->cover_len = cov ? (uint32_t)cov->size() : 0;
+        out->status = r.status;
+        out->num_workers = (uint32_t)r.worker_nodes.size();
+        out->worker_nodes = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, r.worker_nodes.size()) * 8));
+        out->worker_stack_high_water =
+            static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, r.worker_high_water.size()) * 8));
+        for (size_t i = 0; i < r.worker_nodes.size(); ++i) {
+            out->worker_nodes[i] = r.worker_nodes[i];
+            out->worker_stack_high_water[i] = r.worker_high_water[i];
+            out->nodes_total += r.worker_nodes[i];
+        }
+        out->wl_added = r.wl_added;
+        out->wl_removed = r.wl_removed;
+        out->wl_max_size = r.wl_max_size;
+        out->wl_current_size = r.wl_current;
+        out->device_ms = r.device_ms;
+        out->h2d_ms = r.h2d_ms;
+        out->h2d_bytes = r.h2d_bytes;
+        out->d2h_bytes = r.d2h_bytes;
+        out->rounds = r.rounds;
+        out->maxdeg_passes = r.maxdeg;
+        out->children = r.children;
+        out->removals = r.removals;
+        out->degree_bytes = r.degree_bytes;
+        out->n_padded = r.n_padded;
+        out->engine = r.engine;
+        out->grid_blocks = r.grid;
+        out->block_threads = r.block;
+        for (int i = 0; i < 10; ++i) out->phase_cycles[i] = r.phase[i];
+        out->active_cycles = r.active_cycles;
+        out->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return VCG_OK;
+    });
+}
+
+void vcg_result_free(vcg_result* r) {
+    if (!r) return;
+    std::free(r->cover);
+    std::free(r->worker_nodes);
+    std::free(r->worker_stack_high_water);
+    r->cover = nullptr;
+    r->worker_nodes = nullptr;
+    r->worker_stack_high_water = nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// Engine interface between the C-ABI (capi.cpp) and the CUDA side (dense_engine.cu).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "host_graph.hpp"
+
+namespace vcg {
+
+struct SolveSpec {
+    bool pvc = false;
+    uint32_t k = 0;
+    int strategy = 0;           // 0 hybrid, 1 seq, 2 stackonly
+    uint32_t workers = 0;       // 0 = fill the device
+    uint64_t capacity = 4096;
+    uint64_t threshold = 2048;  // worklist_threshold (scheduler.cpp:14-18), computed on host
+    uint32_t depth = 8;
+    uint64_t backoff_us = 50;
+    double timeout_s = -1.0;
+    uint64_t node_budget = 0;
+    int device = 0;
+    int rules = 0;              // 0 reference order, 1 parallel
+    uint32_t block_warps = 0;
+    int engine = 0;
+    bool instrument = false;
+    uint32_t best = 0;          // initial bound: greedy size (MVC, or tighter external) / k (PVC)
+    uint32_t stack_bound = 0;   // stack_bound_for (scheduler.cpp:118-121)
+    const uint32_t* seeds = nullptr;  // [cc, edges, deg[n]] records
+    uint64_t num_seeds = 0;
+    volatile uint32_t* mailbox = nullptr;
+};
+
+struct SolveOut {
+    int status = 0;             // 0 complete, 1 timeout, 2 budget
+    bool found = false;         // a search cover was recorded (MVC: improved; PVC: yes)
+    uint32_t found_size = 0;
+    std::vector<uint32_t> cover;  // internal ids of the recorded cover
+    std::vector<uint64_t> worker_nodes, worker_high_water;
+    uint64_t wl_added = 0, wl_removed = 0, wl_max_size = 0, wl_current = 0;
+    uint64_t rounds = 0, maxdeg = 0, children = 0, removals = 0;
+    uint64_t phase[10] = {0};
+    uint64_t active_cycles = 0;
+    double device_ms = 0, h2d_ms = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    uint32_t degree_bytes = 2, n_padded = 0;
+    int engine = 1;
+    uint32_t grid = 0, block = 0;
+};
+
+// Throws std::runtime_error (CUDA failures) / std::invalid_argument (bad configuration).
+void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out);
+int device_count();
+
+}  // namespace vcg

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA engine (through the C-ABI / public API) against the reference's golden
+answers (tests/golden, generated from the reference itself) and the oracle restatement.
+
+Bar (BASELINE.json north star): bit-exact integer results — the same MVC size, the same PVC
+yes/no, every returned cover verified. Stronger, because the engine applies the reduction
+rules in the reference's order: the 1-worker ("seq") traversal visits exactly the reference's
+solve_seq node count, and PVC no-instance trees are schedule independent, so every worker
+count reproduces the reference node count.
+"""
+import pytest
+
+import paper_2204_10402_b200 as vc
+from paper_2204_10402_b200.configs import load_config
+
+pytestmark = pytest.mark.gpu
+
+
+def graph_of(item):
+    return vc.make_graph(item["n"], [tuple(e) for e in item["edges"]])
+
+
+def check_cover(g, rep):
+    assert len(rep["cover"]) == rep["size"]
+    assert vc.verify_cover(g, rep["cover"]), "certificate is not a vertex cover"
+
+
+def test_device_visible():
+    assert vc.device_count() >= 1
+
+
+def test_corpus_seq_order_is_the_reference_order(corpus):
+    """solve_mvc_seq parity: size AND visited-node count equal the reference (535 graphs)."""
+    bad = []
+    for it in corpus:
+        g = graph_of(it)
+        r = vc.solve_mvc(g, strategy="seq")
+        check_cover(g, r)
+        if r["size"] != it["mvc"] or sum(r["worker_nodes"]) != it["seq_nodes"]:
+            bad.append((it["name"], r["size"], it["mvc"], sum(r["worker_nodes"]), it["seq_nodes"]))
+    assert not bad, bad[:10]
+
+
+def test_corpus_pvc_triple_seq(corpus):
+    bad = []
+    for it in corpus:
+        g = graph_of(it)
+        for p in it["pvc"]:
+            r = vc.solve_pvc(g, p["k"], strategy="seq")
+            ok = r["feasible"] == p["feasible"] and sum(r["worker_nodes"]) == p["nodes"]
+            if r["feasible"]:
+                check_cover(g, r)
+                ok = ok and r["size"] <= p["k"]
+            if not ok:
+                bad.append((it["name"], p, r["feasible"], sum(r["worker_nodes"])))
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("workers,capacity,fraction", [
+    (1, 1, 1.0), (2, 8, 0.25), (4, 64, 0.5), (8, 1, 0.5), (64, 8, 1.0), (None, 4096, 0.5)])
+def test_corpus_hybrid_oracle_equivalence(corpus, workers, capacity, fraction):
+    """acceptance_main.cpp:96-133 over GPU worker counts / capacities / thresholds."""
+    bad = []
+    for it in corpus[::3]:
+        g = graph_of(it)
+        strategy = "gpu" if workers is None else "hybrid"
+        r = vc.solve_mvc(g, strategy=strategy, workers=workers, capacity=capacity,
+                         threshold_fraction=fraction)
+        check_cover(g, r)
+        w = r["worklist"]
+        if (r["size"] != it["mvc"] or r["status"] != "complete" or w["added"] != w["removed"]
+                or w["max_size"] > capacity):
+            bad.append((it["name"], r["size"], it["mvc"], w))
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("workers", [1, 3, 8, None])
+def test_corpus_pvc_triple_hybrid(corpus, workers):
+    """acceptance_main.cpp:135-168; PVC-no node counts are schedule independent."""
+    bad = []
+    for it in corpus[1::4]:
+        g = graph_of(it)
+        for p in it["pvc"]:
+            r = vc.solve_pvc(g, p["k"], strategy="gpu" if workers is None else "hybrid",
+                             workers=workers, capacity=64)
+            ok = r["feasible"] == p["feasible"]
+            if r["feasible"]:
+                check_cover(g, r)
+                ok = ok and r["size"] <= p["k"]
+            else:
+                ok = ok and sum(r["worker_nodes"]) == p["nodes"]
+            if not ok:
+                bad.append((it["name"], p, r["feasible"], sum(r["worker_nodes"])))
+    assert not bad, bad[:10]
+
+
+def test_c1_seq_node_count(config_golden):
+    g = load_config("c1")
+    gold = config_golden["c1"]
+    r = vc.solve_mvc(g, strategy="seq")
+    assert r["size"] == gold["mvc"]
+    assert sum(r["worker_nodes"]) == gold["seq_nodes"]
+    check_cover(g, r)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_config_mvc_and_pvc_pair_full_device(config_golden, name):
+    g = load_config(name)
+    gold = config_golden[name]
+    r = vc.solve_mvc(g, strategy="gpu")
+    assert r["size"] == gold["mvc"] and r["status"] == "complete"
+    check_cover(g, r)
+    no = vc.solve_pvc(g, gold["pvc_no_k"], strategy="gpu")
+    assert not no["feasible"]
+    assert no["nodes_total"] == gold["pvc_no_nodes"]  # schedule-independent tree size
+    yes = vc.solve_pvc(g, gold["mvc"], strategy="gpu")
+    assert yes["feasible"] and yes["size"] <= gold["mvc"]
+    check_cover(g, yes)
+
+
+def test_c5_pvc_no_instance_node_count(config_golden):
+    gold = config_golden["c5"]
+    if "pvc_no_nodes" not in gold:
+        pytest.skip("C5 golden not generated")
+    g = load_config("c5")
+    r = vc.solve_pvc(g, gold["pvc_no_k"], strategy="gpu")
+    assert not r["feasible"] and r["status"] == "complete"
+    assert r["nodes_total"] == gold["pvc_no_nodes"]
+    y = vc.solve_pvc(g, gold["pvc_yes_k"], strategy="gpu")
+    assert y["feasible"] and y["size"] <= gold["pvc_yes_k"]
+    check_cover(g, y)
+
+
+def test_budget_and_timeout_status():
+    g = load_config("c1")
+    r = vc.solve_mvc(g, strategy="gpu", node_budget=1000)
+    assert r["status"] == "budget"
+    check_cover(g, r)  # best-so-far certificate stays valid (test_scheduler.cpp:175-189)
+    r = vc.solve_mvc(g, strategy="hybrid", workers=1, timeout_s=0.0)
+    assert r["status"] == "timeout"
+    check_cover(g, r)
+
+
+def test_report_shape():
+    g = vc.make_graph(10, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (0, 5), (1, 6), (2, 7),
+                           (3, 8), (4, 9), (5, 7), (7, 9), (9, 6), (6, 8), (8, 5)])
+    rep = vc.solve_mvc(g, strategy="hybrid", workers=3)
+    for key in ("n", "m", "mode", "k", "strategy", "workers", "capacity", "threshold_fraction",
+                "depth", "size", "feasible", "cover", "wall_ms", "status", "worker_nodes",
+                "load_ratios", "phase_shares"):
+        assert key in rep
+    assert rep["n"] == 10 and rep["size"] == 6
+    assert len(rep["worker_nodes"]) == 3  # test_smoke.py:64
+    ratios = rep["load_ratios"]
+    assert abs(sum(ratios) / len(ratios) - 1.0) < 1e-9
+    assert sum(rep["phase_shares"].values()) <= 1.0 + 1e-9
+
+
+def test_instrumented_phase_shares():
+    g = load_config("c3")
+    rep = vc.solve_mvc(g, strategy="gpu", instrument=True)
+    assert rep["size"] == 291
+    shares = rep["phase_shares"]
+    assert 0.0 < sum(v for k, v in shares.items() if k != "other") <= 1.0 + 1e-9
