@@ -106,6 +106,9 @@ typedef struct {
     int32_t engine;             /* 0 auto, 1 dense (n <= 1024, warp per node),
                                    2 sparse (any n, CTA per node) */
     int32_t instrument;         /* 1: per-worker phase cycle counters */
+    int32_t donate_oldest;      /* 1: when donating, hand over the OLDEST stacked node (largest
+                                   expected sub-tree) and stack the new child; 0: donate the new
+                                   remove-N(v) child as the reference does (scheduler.cpp:191-199) */
     uint32_t initial_best;      /* MVC: external upper bound (e.g. from another rank),
                                    0 = none; never replaces the greedy certificate */
     /* Seeding (multi-GPU frontier shares): when num_seeds > 0, the worklist starts with these
@@ -139,6 +142,9 @@ typedef struct {
     uint64_t h2d_bytes, d2h_bytes;
     /* roofline counters: rule rounds, max-degree passes, children built */
     uint64_t rounds, maxdeg_passes, children, removals;
+    uint64_t donated;           /* nodes handed to the worklist by workers */
+    uint64_t removals_deg1, removals_deg2, removals_high; /* rule removals, per rule */
+    uint64_t doomed;            /* nodes cut short by the exact high-degree doom test */
     uint32_t degree_bytes;      /* w: bytes per degree entry in the engine's node layout */
     uint32_t n_padded;          /* n rounded to the engine's lane layout */
     int32_t engine;             /* engine that ran: 1 dense, 2 sparse */

@@ -194,7 +194,7 @@ _RULES = {"reference": 0, "parallel": 1}
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
            timeout_s, node_budget, device, rules, block_warps, instrument, initial_best=0,
-           seeds=None, mailbox=None, raw=False):
+           seeds=None, mailbox=None, raw=False, donate_oldest=None):
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
     if workers is None:
@@ -219,6 +219,9 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
     p.rules = _RULES[rules]
     p.block_warps = block_warps
     p.instrument = int(bool(instrument))
+    if donate_oldest is None:  # the tuned GPU policy for "gpu"; the reference policy for "hybrid"
+        donate_oldest = strategy == "gpu"
+    p.donate_oldest = int(bool(donate_oldest))
     p.initial_best = initial_best or 0
     keep = None
     if seeds is not None and len(seeds):
@@ -255,7 +258,9 @@ def _result_dict(r):
         wall_ms=float(r.wall_ms), device_ms=float(r.device_ms), greedy_ms=float(r.greedy_ms),
         h2d_ms=float(r.h2d_ms), h2d_bytes=int(r.h2d_bytes), d2h_bytes=int(r.d2h_bytes),
         rounds=int(r.rounds), maxdeg_passes=int(r.maxdeg_passes), children=int(r.children),
-        removals=int(r.removals), degree_bytes=int(r.degree_bytes), n_padded=int(r.n_padded),
+        removals=int(r.removals), donated=int(r.donated),
+        removals_deg1=int(r.removals_deg1), removals_deg2=int(r.removals_deg2),
+        removals_high=int(r.removals_high), doomed=int(r.doomed), degree_bytes=int(r.degree_bytes), n_padded=int(r.n_padded),
         engine=int(r.engine), grid_blocks=int(r.grid_blocks), block_threads=int(r.block_threads),
         phase_cycles=[int(x) for x in r.phase_cycles], active_cycles=int(r.active_cycles),
     )
@@ -264,20 +269,20 @@ def _result_dict(r):
 def solve_mvc(graph, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
               depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
               rules="reference", block_warps=0, instrument=False, initial_best=0, seeds=None,
-              mailbox=None, raw=False):
+              mailbox=None, raw=False, donate_oldest=None):
     """Solve MVC; returns the run report as a dict (bindings.cpp:174-187)."""
     return _solve(graph, "mvc", 0, strategy, workers, capacity, threshold_fraction, depth,
                   backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  initial_best, seeds, mailbox, raw)
+                  initial_best, seeds, mailbox, raw, donate_oldest)
 
 
 def solve_pvc(graph, k, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
               depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
               rules="reference", block_warps=0, instrument=False, seeds=None, mailbox=None,
-              raw=False):
+              raw=False, donate_oldest=None):
     """Solve PVC for a given k; returns the run report as a dict (bindings.cpp:188-202)."""
     if k < 1:
         raise ValueError("pvc requires k >= 1")  # bindings.cpp:194
     return _solve(graph, "pvc", k, strategy, workers, capacity, threshold_fraction, depth,
                   backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  0, seeds, mailbox, raw)
+                  0, seeds, mailbox, raw, donate_oldest)

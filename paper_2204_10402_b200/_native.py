@@ -27,6 +27,7 @@ class Params(C.Structure):
         ("depth", C.c_uint32), ("backoff_us", C.c_uint64), ("timeout_s", C.c_double),
         ("node_budget", C.c_uint64), ("device", C.c_int32), ("rules", C.c_int32),
         ("block_warps", C.c_uint32), ("engine", C.c_int32), ("instrument", C.c_int32),
+        ("donate_oldest", C.c_int32),
         ("initial_best", C.c_uint32), ("num_seeds", C.c_uint64),
         ("seeds", C.POINTER(C.c_uint32)), ("mailbox", C.POINTER(C.c_uint32)),
     ]
@@ -45,7 +46,10 @@ class Result(C.Structure):
         ("wl_current_size", C.c_uint64), ("wall_ms", C.c_double), ("device_ms", C.c_double),
         ("greedy_ms", C.c_double), ("h2d_ms", C.c_double), ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64), ("rounds", C.c_uint64), ("maxdeg_passes", C.c_uint64),
-        ("children", C.c_uint64), ("removals", C.c_uint64), ("degree_bytes", C.c_uint32),
+        ("children", C.c_uint64), ("removals", C.c_uint64), ("donated", C.c_uint64),
+        ("removals_deg1", C.c_uint64), ("removals_deg2", C.c_uint64),
+        ("removals_high", C.c_uint64), ("doomed", C.c_uint64),
+        ("degree_bytes", C.c_uint32),
         ("n_padded", C.c_uint32), ("engine", C.c_int32), ("grid_blocks", C.c_uint32),
         ("block_threads", C.c_uint32), ("phase_cycles", C.c_uint64 * 10),
         ("active_cycles", C.c_uint64),

@@ -221,6 +221,7 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         s.block_warps = p->block_warps;
         s.engine = p->engine;
         s.instrument = p->instrument != 0;
+        s.donate_oldest = p->donate_oldest != 0;
         s.best = pvc ? p->k : greedy.size;
         if (!pvc && p->initial_best && p->initial_best < s.best) s.best = p->initial_best;
         // stack_bound_for (scheduler.cpp:118-121)
@@ -286,6 +287,11 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         out->maxdeg_passes = r.maxdeg;
         out->children = r.children;
         out->removals = r.removals;
+        out->donated = r.donated;
+        out->removals_deg1 = r.rm1;
+        out->removals_deg2 = r.rm2;
+        out->removals_high = r.rmh;
+        out->doomed = r.dooms;
         out->degree_bytes = r.degree_bytes;
         out->n_padded = r.n_padded;
         out->engine = r.engine;

@@ -58,26 +58,29 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 // ------------------------------------------------------------------ device-global state
 
 struct Ctl {
-    // line 0: read by every worker once per node as one 16-byte load
+    // line 0: read by every worker once per node (two vector loads)
     uint32_t best;    // MVC bound (atomicMin); PVC: k
     uint32_t cancel;  // 1 = stop: PVC found, timeout, budget, host request
-    int32_t wl_size;  // reserved worklist slots
     uint32_t found;   // PVC: a cover of size <= k was recorded
-    uint32_t pad0[28];
-    // line 1: queue tickets + termination counter
+    uint32_t pad0;
+    // (pending << 32) | size: pending = queued items + active workers (termination when 0);
+    // size = queued items + in-flight enqueue reservations (threshold gate, capacity)
+    unsigned long long work;
+    unsigned long long pad1;
+    uint32_t pad2[24];
+    // line 1: ring tickets (Vyukov-style slots with per-slot sequence numbers)
     unsigned long long head, tail;
-    int32_t avail;    // published, unclaimed items
-    int32_t pending;  // queued items + active workers
-    uint32_t pad1[26];
-    // line 2: statistics / results
-    unsigned long long added, removed, nodes_total, best_owner;
-    int32_t max_size, status;
-    uint32_t pad2[22];
+    uint32_t pad3[28];
+    // line 2: results
+    unsigned long long nodes_total, best_owner;
+    int32_t status;
+    uint32_t pad4[27];
 };
 static_assert(sizeof(Ctl) == 384, "Ctl layout");
 
 struct WStats {
-    unsigned long long nodes, rounds, maxdeg, children, removals, high_water, donated, active;
+    unsigned long long nodes, rounds, maxdeg, children, rm1, rm2, rmh, high_water, donated,
+        active, max_queue, dooms;
     unsigned long long phase[10];
 };
 
@@ -89,13 +92,15 @@ struct DenseArgs {
     uint32_t n, npad, m;
     int pvc;
     uint32_t k;
-    uint32_t capacity, threshold;
+    uint32_t capacity;        // logical worklist capacity (try_add rejects at capacity)
+    uint32_t ring_mask;       // physical ring slots - 1 (power of two >= max(capacity, 2))
+    uint32_t threshold;
     uint32_t workers;
     uint32_t stack_bound;
     unsigned long long entry_bytes;
     unsigned char* stacks;    // workers * stack_bound * entry_bytes
-    unsigned char* wl;        // capacity * entry_bytes
-    unsigned long long* seq;  // capacity
+    unsigned char* wl;        // ring slots * entry_bytes
+    unsigned long long* seq;  // ring slots
     Ctl* ctl;
     uint32_t* cover_slots;    // workers * W words
     WStats* stats;
@@ -104,6 +109,7 @@ struct DenseArgs {
     unsigned long long flush_every;  // visits between node-counter flushes / limit checks
     uint32_t backoff_ns;
     int seq_mode;             // never donate (solve_*_seq semantics)
+    int donate_oldest;        // donate the bottom (oldest) stack entry instead of the new child
     volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out, [3] found out
 };
 
@@ -120,6 +126,16 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ld_volatile_v2u64(const void* p) {
+    ulonglong2 r;
+    asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
 }
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
     unsigned long long v;
@@ -173,6 +189,7 @@ struct WarpNode {
     uint32_t d[W];                   // degree of vertex 32*i + lane
     uint32_t aw;                     // lane j < W: alive bitmap word j
     uint32_t cc, edges;              // uniform
+    bool doom;                       // uniform: proven to be pruned (see pass_high)
     const uint4* sat;                // shared adjacency bitmap
     uint32_t npad;
     int lane;
@@ -244,10 +261,16 @@ struct WarpNode {
         return 32 * j + __ffs(w) - 1;
     }
     // reductions.cpp:7-19
-    __device__ __forceinline__ bool pass_degree_one(unsigned long long& removals) {
+    // A node whose cover already reaches the bound is pruned whatever the remaining rules do
+    // (should_prune tests |S| first and rules only grow S), so the reduction may stop there.
+    __device__ __forceinline__ bool doomed(int pvc, uint32_t k, uint32_t snap) const {
+        return doom || (pvc ? cc > k : cc >= snap);
+    }
+    __device__ __forceinline__ bool pass_degree_one(unsigned long long& removals, int pvc,
+                                                    uint32_t k, uint32_t snap) {
         bool changed = false;
         int pos = 0;
-        while (true) {
+        while (!doomed(pvc, k, snap)) {
             int v = find_first(pos, [](uint32_t x) { return x == 1u; });
             if (v < 0) break;
             int u = first_bit(alive_row(v));
@@ -259,10 +282,11 @@ struct WarpNode {
         return changed;
     }
     // reductions.cpp:22-40 (partners = the two alive neighbours, ascending)
-    __device__ __forceinline__ bool pass_degree_two(unsigned long long& removals) {
+    __device__ __forceinline__ bool pass_degree_two(unsigned long long& removals, int pvc,
+                                                    uint32_t k, uint32_t snap) {
         bool changed = false;
         int pos = 0;
-        while (true) {
+        while (!doomed(pvc, k, snap)) {
             int v = find_first(pos, [](uint32_t x) { return x == 2u; });
             if (v < 0) break;
             const uint32_t xl = alive_row(v);
@@ -295,7 +319,20 @@ struct WarpNode {
         bool changed = false;
         int pos = 0;
         uint32_t lim = limit_for(pvc, k, snap, cc);
-        while (true) {
+        // Every alive vertex above the limit at pass start is removed by this pass (each
+        // removal lowers the limit by one and a degree by at most one), so more than `lim` of
+        // them take |S| past the bound: the node is pruned whatever else happens.
+        uint32_t over = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t x = d[i];
+            over += __popc(__ballot_sync(FULL, x != REM && x > 0u && x > lim));
+        }
+        if (over > lim) {
+            doom = true;
+            return true;
+        }
+        while (!doomed(pvc, k, snap)) {
             int v = find_first(pos, [lim](uint32_t x) { return x != REM && x > 0u && x > lim; });
             if (v < 0) break;
             remove_vertex(v);
@@ -307,7 +344,8 @@ struct WarpNode {
         return changed;
     }
     // reduce_loop (reductions.cpp:63-90) with the bound snapshot taken per round
-    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, WStats& st) {
+    template <class Cnt>
+    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st) {
         while (true) {
             if (edges == 0) break;
             ++st.rounds;
@@ -323,18 +361,18 @@ struct WarpNode {
             if (!any) break;
             bool changed = false;
             long long t0 = INSTR ? clock64() : 0;
-            changed |= pass_degree_one(st.removals);
+            changed |= pass_degree_one(st.rm1, pvc, k, snap);
             long long t1 = INSTR ? clock64() : 0;
-            changed |= pass_degree_two(st.removals);
+            changed |= pass_degree_two(st.rm2, pvc, k, snap);
             long long t2 = INSTR ? clock64() : 0;
-            changed |= pass_high(pvc, k, snap, st.removals);
+            changed |= pass_high(pvc, k, snap, st.rmh);
             if (INSTR) {
                 long long t3 = clock64();
                 st.phase[PH_DEG1] += t1 - t0;
                 st.phase[PH_DEG2] += t2 - t1;
                 st.phase[PH_HIGH] += t3 - t2;
             }
-            if (!changed) break;
+            if (!changed || doomed(pvc, k, snap)) break;
         }
     }
     // search_node.cpp:34-46: smallest id among alive vertices of maximum degree
@@ -400,7 +438,19 @@ struct WarpNode {
                     make_uint4(packed[4 * t], packed[4 * t + 1], packed[4 * t + 2], packed[4 * t + 3]);
         }
     }
-    // Full copy of the current node (used only when a node must be parked as-is).
+    // Moves one record (header + lane-major degrees) between stack and worklist memory.
+    __device__ __forceinline__ void copy_record(const unsigned char* src, unsigned char* dst) const {
+        const unsigned char* p = src + 16 + lane * (2 * W);
+        unsigned char* q = dst + 16 + lane * (2 * W);
+        if constexpr (W == 4) {
+            *reinterpret_cast<uint2*>(q) = *reinterpret_cast<const uint2*>(p);
+        } else {
+#pragma unroll
+            for (int t = 0; t < W / 8; ++t)
+                reinterpret_cast<uint4*>(q)[t] = reinterpret_cast<const uint4*>(p)[t];
+        }
+        if (lane == 0) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    }
     template <bool CG>
     __device__ __forceinline__ void load(const unsigned char* rec) {
         uint32_t packed[W / 2];
@@ -429,6 +479,7 @@ struct WarpNode {
         }
         cc = __shfl_sync(FULL, h0, 0);
         edges = __shfl_sync(FULL, h1, 0);
+        doom = false;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const uint32_t h = (i & 1) ? (packed[i / 2] >> 16) : (packed[i / 2] & 0xFFFFu);
@@ -438,8 +489,33 @@ struct WarpNode {
     }
 };
 
+constexpr unsigned long long ONE_PENDING = 1ull << 32;
+
+// GlobalWorklist::try_add (worklist.cpp:11-19): reserve capacity in the packed word (also
+// counting the item in `pending` before it can be seen), then draw a ticket. Two always-
+// succeeding atomics; no CAS loops (they collapse under thousands of contending warps).
+__device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long& pos_out,
+                                          unsigned long long& size_seen) {
+    Ctl* ctl = a.ctl;
+    const unsigned long long old = atomicAdd(&ctl->work, ONE_PENDING | 1ull);
+    const uint32_t size = (uint32_t)old;
+    if (size >= a.capacity) {
+        atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);  // undo (try_add rejects)
+        return false;
+    }
+    size_seen = size + 1ull;
+    pos_out = atomicAdd(&ctl->tail, 1ull);
+    return true;
+}
+
+struct Counters {
+    unsigned long long nodes = 0, rounds = 0, maxdeg = 0, children = 0, rm1 = 0, rm2 = 0,
+                       rmh = 0, high_water = 0, donated = 0, max_queue = 0, dooms = 0;
+    unsigned long long phase[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+};
+
 template <int W, bool INSTR>
-__global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
+__global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_kernel(DenseArgs a) {
     extern __shared__ uint4 sat[];
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
@@ -457,16 +533,21 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
     x.sat = sat;
     x.npad = a.npad;
     x.lane = lane;
-    WStats st;
-    memset(&st, 0, sizeof(st));
+    Counters st;
     Ctl* ctl = a.ctl;
-    unsigned char* my_stack = a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes;
-    uint32_t sp = 0;
+    unsigned char* const my_stack =
+        a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes;
+    // The local stack is a ring [base, base + sp) so the oldest entry can be donated.
+    uint32_t base = 0, sp = 0;
+    auto slot_at = [&](uint32_t i) {
+        uint32_t j = base + i;
+        if (j >= a.stack_bound) j -= a.stack_bound;
+        return my_stack + (unsigned long long)j * a.entry_bytes;
+    };
     bool have = false, idle = true;
     uint32_t best = a.pvc ? a.k : ctl->best;
     unsigned long long nodes_flushed = 0;
-    const uint32_t last_word_mask =
-        (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : FULL;
+    const uint32_t last_word_mask = (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : FULL;
     const int last_word = (int)((a.n + 31) / 32) - 1;
 
     while (true) {
@@ -474,60 +555,50 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
             if (sp > 0) {
                 long long t0 = INSTR ? clock64() : 0;
                 --sp;
-                x.template load<false>(my_stack + (unsigned long long)sp * a.entry_bytes);
+                x.template load<false>(slot_at(sp));
                 have = true;
                 if (INSTR) st.phase[PH_STACK] += clock64() - t0;
             } else {
                 // GlobalWorklist::remove_or_done (worklist.cpp:21-48) on the device ring
                 long long t0 = INSTR ? clock64() : 0;
                 if (!idle) {
-                    if (lane == 0) atomicSub(&ctl->pending, 1);
+                    if (lane == 0) atomicAdd(&ctl->work, ~ONE_PENDING + 1ull);  // pending - 1
                     idle = true;
                 }
-                uint32_t sleep = 64;
-                int outcome = 0;  // 1 got, 2 done
+                // take a ticket, then wait for that slot to be published, for termination
+                // (pending == 0) or for a cancel
                 unsigned long long pos = 0;
-                while (outcome == 0) {
+                if (lane == 0) pos = atomicAdd(&ctl->head, 1ull);
+                pos = __shfl_sync(FULL, pos, 0);
+                unsigned long long* sq = a.seq + (pos & a.ring_mask);
+                uint32_t sleep = 32;
+                int outcome = 0;  // 1 got, 2 done
+                for (uint32_t spin = 0;; ++spin) {
                     int o = 0;
-                    unsigned long long p = 0;
                     if (lane == 0) {
-                        const uint4 h = ld_volatile_v4(ctl);
-                        if (h.y) {
-                            o = 2;
-                        } else if (ld_relaxed_s32(&ctl->avail) > 0) {
-                            if (atomicSub(&ctl->avail, 1) > 0) {
-                                p = atomicAdd(&ctl->head, 1ull);
-                                o = 1;
-                            } else {
-                                atomicAdd(&ctl->avail, 1);
-                            }
+                        if (ld_acquire_u64(sq) == pos + 1) o = 1;
+                        else if ((spin & 7) == 7) {
+                            if (ld_volatile_v4(ctl).y) o = 2;
+                            else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0) o = 2;
+                            else if (worker == 0 && a.mailbox) poll_mailbox(a, ctl);
                         }
-                        if (o == 0 && ld_relaxed_s32(&ctl->pending) == 0) o = 2;
-                        if (o == 0 && worker == 0 && a.mailbox) poll_mailbox(a, ctl);
                     }
                     outcome = __shfl_sync(FULL, o, 0);
-                    pos = __shfl_sync(FULL, p, 0);
-                    if (outcome == 0) {
-                        __nanosleep(sleep);
-                        sleep = min(sleep * 2, a.backoff_ns);
-                    }
+                    if (outcome) break;
+                    __nanosleep(sleep);
+                    sleep = min(sleep * 2, a.backoff_ns);
                 }
                 if (outcome == 2) {
                     if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
                     break;
                 }
-                const uint32_t slot = (uint32_t)(pos % a.capacity);
-                if (lane == 0)
-                    while (ld_acquire_u64(a.seq + slot) != pos + 1) __nanosleep(32);
-                __syncwarp();
-                (void)ld_acquire_u64(a.seq + slot);  // every lane acquires before reading
-                x.template load<true>(a.wl + (unsigned long long)slot * a.entry_bytes);
+                (void)ld_acquire_u64(sq);  // every lane acquires the publication before reading
+                x.template load<true>(a.wl + (pos & a.ring_mask) * a.entry_bytes);
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) {
-                    st_release_u64(a.seq + slot, pos + a.capacity);
-                    atomicSub(&ctl->wl_size, 1);
-                    atomicAdd(&ctl->removed, 1ull);
+                    st_release_u64(sq, pos + a.ring_mask + 1);  // free for the next lap
+                    atomicAdd(&ctl->work, ~0ull);                // size - 1 (pending unchanged)
                 }
                 idle = false;
                 have = true;
@@ -535,15 +606,19 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
             }
         }
 
-        // one 16-byte read per node: {best, cancel, wl_size, found}
-        uint4 h = make_uint4(0, 0, 0, 0);
-        if (lane == 0) h = ld_volatile_v4(ctl);
-        const uint32_t cancel = __shfl_sync(FULL, h.y, 0);
-        if (cancel) break;
-        if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
-        const int wl_size = __shfl_sync(FULL, (int)h.z, 0);
+        // Issue the read of the hot control line ({best, cancel} + queue size) now and consume
+        // it after the reduction, so its L2 latency hides behind the rule passes. The rules use
+        // the bound seen at the previous node (a stale, larger bound only prunes less).
+        uint32_t h_best = 0, h_cancel = 0;
+        unsigned long long h_size = 0;
+        if (lane == 0) {
+            const uint4 h = ld_volatile_v4(ctl);
+            h_best = h.x;
+            h_cancel = h.y;
+            h_size = (uint32_t)ld_relaxed_u64(&ctl->work);
+        }
 
-        // visit_and_check_limits (scheduler.cpp:63-74), batched: one atomic per 64 visits
+        // visit_and_check_limits (scheduler.cpp:63-74), batched: one atomic per flush_every visits
         ++st.nodes;
         if (st.nodes - nodes_flushed >= a.flush_every) {
             int stop = 0;
@@ -564,9 +639,13 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
 
         // process_node (scheduler.cpp:125-144)
         x.reduce(a.pvc, a.k, best, st);
+        if (__shfl_sync(FULL, h_cancel, 0)) break;
+        if (!a.pvc) best = min(best, __shfl_sync(FULL, h_best, 0));
+        const unsigned long long qsize = __shfl_sync(FULL, h_size, 0);
         long long tp = INSTR ? clock64() : 0;
-        const bool prune = should_prune(a.pvc, a.k, best, x.cc, x.edges);
+        const bool prune = x.doom || should_prune(a.pvc, a.k, best, x.cc, x.edges);
         if (INSTR) st.phase[PH_PRUNE] += clock64() - tp;
+        st.dooms += x.doom;
         if (prune) {
             have = false;
             continue;
@@ -574,35 +653,13 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
         if (x.edges == 0) {
             // record_cover (scheduler.cpp:84-108)
             uint32_t* slot = a.cover_slots + (unsigned long long)worker * W;
-            if (a.pvc) {
-                uint32_t first = 0;
-                if (lane == 0) first = atomicCAS(&ctl->found, 0u, 1u) == 0u;
-                first = __shfl_sync(FULL, first, 0);
-                if (first) {
-#pragma unroll
-                    for (int i = 0; i < W; ++i) {
-                        uint32_t b = __ballot_sync(FULL, x.d[i] == REM);
-                        b = i < last_word ? b : (i == last_word ? (b & last_word_mask) : 0u);
-                        if (lane == i) slot[i] = b;
-                    }
-                    __threadfence();
-                    __syncwarp();
-                    if (lane == 0) {
-                        atomicMin(&ctl->best_owner,
-                                  ((unsigned long long)x.cc << 32) | worker);
-                        atomicExch(&ctl->cancel, 1u);
-                        if (a.mailbox) {
-                            a.mailbox[2] = x.cc;
-                            a.mailbox[3] = 1;
-                        }
-                    }
-                }
-                break;
+            uint32_t record = 0;
+            if (lane == 0) {
+                if (a.pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
+                else record = x.cc < atomicMin(&ctl->best, x.cc);
             }
-            uint32_t old = 0;
-            if (lane == 0) old = atomicMin(&ctl->best, x.cc);
-            old = __shfl_sync(FULL, old, 0);
-            if (x.cc < old) {
+            record = __shfl_sync(FULL, record, 0);
+            if (record) {
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
                     uint32_t b = __ballot_sync(FULL, x.d[i] == REM);
@@ -613,9 +670,14 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
                 __syncwarp();
                 if (lane == 0) {
                     atomicMin(&ctl->best_owner, ((unsigned long long)x.cc << 32) | worker);
-                    if (a.mailbox) a.mailbox[2] = x.cc;
+                    if (a.pvc) atomicExch(&ctl->cancel, 1u);
+                    if (a.mailbox) {
+                        a.mailbox[2] = x.cc;
+                        if (a.pvc) a.mailbox[3] = 1;
+                    }
                 }
             }
+            if (a.pvc) break;  // the search is ended (solver_seq.cpp:108)
             best = min(best, x.cc);
             have = false;
             continue;
@@ -625,48 +687,46 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
         ++st.maxdeg;
         if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
 
-        // branch: defer remove-N(v) (donate below threshold, else stack), continue with remove-v
+        // Branch (scheduler.cpp:185-203): defer remove-N(v) — donated while the worklist is
+        // below its threshold (optionally the oldest stacked node goes instead) — and continue
+        // with remove-v.
         long long tb = INSTR ? clock64() : 0;
-        bool donated = false;
-        if (!a.seq_mode && wl_size < (int)a.threshold) {
-            unsigned long long pos = 0;
+        bool child_placed = false;
+        if (!a.seq_mode && qsize < a.threshold) {
+            unsigned long long pos = 0, seen = 0;
             int ok = 0;
-            if (lane == 0) {
-                const int old = atomicAdd(&ctl->wl_size, 1);
-                if (old >= (int)a.capacity) {
-                    atomicSub(&ctl->wl_size, 1);
-                } else {
-                    ok = 1;
-                    atomicAdd(&ctl->pending, 1);
-                    pos = atomicAdd(&ctl->tail, 1ull);
-                    atomicMax(&ctl->max_size, old + 1);
-                }
-            }
+            if (lane == 0) ok = q_reserve(a, pos, seen);
             ok = __shfl_sync(FULL, ok, 0);
             if (ok) {
                 pos = __shfl_sync(FULL, pos, 0);
-                const uint32_t slot = (uint32_t)(pos % a.capacity);
-                if (lane == 0)
-                    while (ld_acquire_u64(a.seq + slot) != pos) __nanosleep(32);
+                if (lane == 0) {
+                    st.max_queue = max(st.max_queue, seen);
+                    // the slot is free once the previous lap's reader released it
+                    while (ld_acquire_u64(a.seq + (pos & a.ring_mask)) != pos) __nanosleep(32);
+                }
                 __syncwarp();
-                x.write_child_without_neighbors(v, a.wl + (unsigned long long)slot * a.entry_bytes);
+                unsigned char* dst = a.wl + (pos & a.ring_mask) * a.entry_bytes;
+                if (a.donate_oldest && sp > 0) {
+                    x.copy_record(slot_at(0), dst);
+                    base = base + 1 == a.stack_bound ? 0 : base + 1;
+                    --sp;
+                } else {
+                    x.write_child_without_neighbors(v, dst);
+                    child_placed = true;
+                }
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) {
-                    st_release_u64(a.seq + slot, pos + 1);
-                    atomicAdd(&ctl->avail, 1);
-                    atomicAdd(&ctl->added, 1ull);
-                }
-                donated = true;
+                if (lane == 0) st_release_u64(a.seq + (pos & a.ring_mask), pos + 1);
                 ++st.donated;
                 if (INSTR) st.phase[PH_WL_ADD] += clock64() - tb;
             }
         }
-        if (!donated) {
-            x.write_child_without_neighbors(v, my_stack + (unsigned long long)sp * a.entry_bytes);
+        if (!child_placed) {
+            long long ts = INSTR ? clock64() : 0;
+            x.write_child_without_neighbors(v, slot_at(sp));
             ++sp;
             if (sp > st.high_water) st.high_water = sp;
-            if (INSTR) st.phase[PH_BRANCH_NBRS] += clock64() - tb;
+            if (INSTR) st.phase[PH_BRANCH_NBRS] += clock64() - ts;
         }
         ++st.children;
         long long tv = INSTR ? clock64() : 0;
@@ -676,9 +736,23 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
 
     if (lane == 0) {
         if (st.nodes > nodes_flushed) atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed);
+        WStats o;
+        o.nodes = st.nodes;
+        o.rounds = st.rounds;
+        o.maxdeg = st.maxdeg;
+        o.children = st.children;
+        o.rm1 = st.rm1;
+        o.rm2 = st.rm2;
+        o.rmh = st.rmh;
+        o.dooms = st.dooms;
+        o.high_water = st.high_water;
+        o.donated = st.donated;
+        o.active = clock64() - c_start;
+        o.max_queue = st.max_queue;
+#pragma unroll
+        for (int p = 0; p < 10; ++p) o.phase[p] = st.phase[p];
+        a.stats[worker] = o;
         (void)t_start;
-        st.active = clock64() - c_start;
-        a.stats[worker] = st;
     }
 }
 
@@ -734,8 +808,8 @@ DeviceCtx& ctx_for(int dev) {
     return *g_ctx[dev];
 }
 
-__global__ void init_seq_kernel(unsigned long long* seq, uint32_t cap, uint32_t filled) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x)
+__global__ void init_seq_kernel(unsigned long long* seq, uint32_t ring, uint32_t filled) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ring; i += gridDim.x * blockDim.x)
         seq[i] = i < filled ? i + 1ull : (unsigned long long)i;
 }
 
@@ -860,18 +934,20 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     // memory: stacks, worklist ring, control, cover slots, stats
     const uint32_t bound = std::max<uint32_t>(s.stack_bound, 1) + 1;
     const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(s.capacity, s.num_seeds), 1);
-    if (cap > 0x7FFFFFFF) throw std::invalid_argument("worklist capacity too large");
+    if (cap > (1ull << 30)) throw std::invalid_argument("worklist capacity too large");
+    uint64_t ring = 2;
+    while (ring < cap) ring <<= 1;
     const size_t stack_bytes = (size_t)workers * bound * entry;
-    const size_t wl_bytes = (size_t)cap * entry;
+    const size_t wl_bytes = (size_t)ring * entry;
     unsigned char* stacks = (unsigned char*)C.stacks.get(stack_bytes);
     unsigned char* wl = (unsigned char*)C.wl.get(wl_bytes);
-    unsigned long long* seq = (unsigned long long*)C.seq.get(cap * 8);
-    const size_t misc_bytes = sizeof(Ctl) + (size_t)workers * W * 4 + (size_t)workers * sizeof(WStats) + 256;
+    unsigned long long* seq = (unsigned long long*)C.seq.get(ring * 8);
+    const size_t slots_bytes = (((size_t)workers * W * 4) + 255) / 256 * 256;
+    const size_t misc_bytes = sizeof(Ctl) + slots_bytes + (size_t)workers * sizeof(WStats);
     unsigned char* misc = (unsigned char*)C.misc.get(misc_bytes);
     Ctl* ctl = reinterpret_cast<Ctl*>(misc);
     uint32_t* cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
-    WStats* stats = reinterpret_cast<WStats*>(
-        misc + ((sizeof(Ctl) + (size_t)workers * W * 4 + 15) / 16) * 16);
+    WStats* stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
 
     // initial worklist content: the root (init_root, search_node.cpp:7-14) or the seeds
     const uint64_t nseeds = s.num_seeds ? s.num_seeds : 1;
@@ -889,16 +965,13 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     Ctl hc;
     std::memset(&hc, 0, sizeof(hc));
     hc.best = s.best;
-    hc.wl_size = (int32_t)nseeds;
+    hc.head = 0;
     hc.tail = nseeds;
-    hc.avail = (int32_t)nseeds;
-    hc.pending = (int32_t)nseeds;
-    hc.added = nseeds;
-    hc.max_size = (int32_t)nseeds;
+    hc.work = (nseeds << 32) | nseeds;
     hc.best_owner = ~0ull;
     CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, C.stream));
     CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, C.stream));
-    init_seq_kernel<<<64, 256, 0, C.stream>>>(seq, (uint32_t)cap, (uint32_t)nseeds);
+    init_seq_kernel<<<64, 256, 0, C.stream>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
     CUDA_CHECK(cudaGetLastError());
     CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), C.stream));
     out.h2d_bytes += sizeof(hc) + recs.size();
@@ -913,6 +986,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     a.pvc = s.pvc ? 1 : 0;
     a.k = s.k;
     a.capacity = (uint32_t)cap;
+    a.ring_mask = (uint32_t)(ring - 1);
     a.threshold = (uint32_t)std::min<uint64_t>(s.threshold, cap);
     a.workers = workers;
     a.stack_bound = bound;
@@ -928,8 +1002,11 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
     a.flush_every = 64;
     if (s.node_budget) a.flush_every = std::max<uint64_t>(1, std::min<uint64_t>(64, s.node_budget / (4ull * workers)));
-    a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 1000000);
+    // idle back-off: exponential from 32 ns, capped at backoff_us (at most 2 us on the device —
+    // a polling warp costs one L2 read, an over-sleeping one leaves queued work unclaimed)
+    a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
     a.seq_mode = s.strategy == 1 ? 1 : 0;
+    a.donate_oldest = s.donate_oldest ? 1 : 0;
     a.mailbox = s.mailbox;
 
     CUDA_CHECK(cudaEventRecord(C.ev0, C.stream));
@@ -952,10 +1029,10 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     CUDA_CHECK(cudaMemcpy(hs.data(), stats, workers * sizeof(WStats), cudaMemcpyDeviceToHost));
     out.d2h_bytes += sizeof(hc) + workers * sizeof(WStats);
     out.status = hc.status;
-    out.wl_added = hc.added;
-    out.wl_removed = hc.removed;
-    out.wl_max_size = (uint64_t)std::max(hc.max_size, 0);
-    out.wl_current = (uint64_t)std::max(hc.wl_size, 0);
+    out.wl_added = hc.tail;  // every enqueue ticket is one added node (root/seeds included)
+    out.wl_current = (uint32_t)hc.work;
+    out.wl_removed = hc.tail - out.wl_current;
+    out.wl_max_size = nseeds;
     out.worker_nodes.resize(workers);
     out.worker_high_water.resize(workers);
     for (uint32_t w = 0; w < workers; ++w) {
@@ -964,8 +1041,14 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
         out.rounds += hs[w].rounds;
         out.maxdeg += hs[w].maxdeg;
         out.children += hs[w].children;
-        out.removals += hs[w].removals;
+        out.removals += hs[w].rm1 + hs[w].rm2 + hs[w].rmh;
+        out.rm1 += hs[w].rm1;
+        out.rm2 += hs[w].rm2;
+        out.rmh += hs[w].rmh;
+        out.dooms += hs[w].dooms;
+        out.donated += hs[w].donated;
         out.active_cycles += hs[w].active;
+        out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
         for (int p = 0; p < 10; ++p) out.phase[p] += hs[w].phase[p];
     }
     if (hc.best_owner != ~0ull) {

@@ -25,6 +25,7 @@ struct SolveSpec {
     uint32_t block_warps = 0;
     int engine = 0;
     bool instrument = false;
+    bool donate_oldest = false;
     uint32_t best = 0;          // initial bound: greedy size (MVC, or tighter external) / k (PVC)
     uint32_t stack_bound = 0;   // stack_bound_for (scheduler.cpp:118-121)
     const uint32_t* seeds = nullptr;  // [cc, edges, deg[n]] records
@@ -39,7 +40,8 @@ struct SolveOut {
     std::vector<uint32_t> cover;  // internal ids of the recorded cover
     std::vector<uint64_t> worker_nodes, worker_high_water;
     uint64_t wl_added = 0, wl_removed = 0, wl_max_size = 0, wl_current = 0;
-    uint64_t rounds = 0, maxdeg = 0, children = 0, removals = 0;
+    uint64_t rounds = 0, maxdeg = 0, children = 0, removals = 0, donated = 0;
+    uint64_t rm1 = 0, rm2 = 0, rmh = 0, dooms = 0;
     uint64_t phase[10] = {0};
     uint64_t active_cycles = 0;
     double device_ms = 0, h2d_ms = 0;
