@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py — headline measurement (driver contract).
+
+Workload (BASELINE.json metric "time-to-solution and search-tree nodes/sec at 1/2/4/8 B200 vs
+CPU ref"): config C5, the hard PVC no-instance — k = MVC-1 = 482 on the complement of the
+p_hat-style G(500, a=.25, b=.75) seed-0 graph (data/configs/c5.clq.gz, n=500, m=61,209). One
+step = one complete exact solve (the whole 21,461,369-node search tree; answer "no").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torchrun, one process per GPU: a deterministic device frontier expansion on
+every rank, then each rank's share on its own GPU (strong scaling, max-over-ranks time).
+`--impl reference` times the reference's own CPU solver (oracle/_ref/libvcref.so, run_hybrid
+with every host thread) on bounded samples of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-solution and search-tree nodes/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "nodes/s"
+WORKLOAD = ("C5: PVC k=482 (=MVC-1, no-instance) on the complement of p_hat-style "
+            "G(500, a=0.25, b=0.75) seed 0")
+K_NO = 482
+C5_NODES = 21461369  # reference node count (tests/golden/configs.json)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--frontier-per-rank", type=int, default=1024)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def csr_of(graph):
+    off, nbr = graph.csr()
+    return off, nbr
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dense_kernel_c5", {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- reference (CPU) arm
+
+def reference_line(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import CSR, Reference
+    from paper_2204_10402_b200.configs import config_text
+    ref = Reference()
+    g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
+    cores = os.cpu_count() or 1
+    budget_s = max(2.0, min(12.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=1.0)
+    rates, nodes = [], 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=budget_s)
+        rates.append(r["nodes"] / (r["wall_ms"] / 1e3))
+        nodes += r["nodes"]
+    wall = time.perf_counter() - t0
+    value = nodes / wall
+    sample = (f"reference run_hybrid ({cores} threads) on C5 PVC k={K_NO}, each step the first "
+              f"{budget_s:.1f} s of the same search (timeout); full tree {C5_NODES} nodes")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
+        "config": {"workload": WORKLOAD, "n": g.n, "m": g.m, "k": K_NO, "threads": cores},
+        "time_to_solution_s_est": C5_NODES / value,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline(sample_s):
+    """The reference on the box's host cores, bounded sample (rank 0, N=1 only)."""
+    try:
+        from oracle.oracle import Reference
+        from paper_2204_10402_b200.configs import config_text
+        ref = Reference()
+    except OSError as e:
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
+    cores = os.cpu_count() or 1
+    r = ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=sample_s)
+    return {"value": r["nodes"] / (r["wall_ms"] / 1e3), "unit": UNIT, "cores": cores,
+            "kind": "reference",
+            "sample": (f"reference run_hybrid, {cores} threads, C5 PVC k={K_NO}: "
+                       f"{r['nodes']} nodes in {r['wall_ms'] / 1e3:.1f} s "
+                       f"(status {r['status']}; full tree {C5_NODES} nodes)")}
+
+
+# ---------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_line(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2204_10402_b200 as vc
+    from paper_2204_10402_b200.configs import load_config
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        xg = dist.new_group(backend="gloo")
+    stream = torch.cuda.Stream()  # the library launches on this stream; events bracket it
+    g = load_config("c5")
+    n, m = g.num_vertices, g.num_edges
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step():
+        if world == 1:
+            r = vc.solve_pvc(g, K_NO, strategy="gpu", device=local, stream=stream.cuda_stream)
+            r["rank_nodes"] = [r["nodes_total"]]
+            return r
+        from paper_2204_10402_b200.distributed import solve_distributed
+        return solve_distributed(g, "pvc", K_NO, exchange_group=xg, device=local,
+                                 stream=stream.cuda_stream,
+                                 frontier_per_rank=args.frontier_per_rank)
+
+    for _ in range(args.warmup):
+        r = step()
+        assert not r["feasible"], "C5 k=482 must be infeasible"
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(step())
+            flush.zero_()  # L2 flush between timed steps (inside the bracket; ~0.05 ms)
+        ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    for r in results:
+        assert not r["feasible"] and r["status"] == "complete"
+    nodes_per_step = results[-1]["nodes_total"]
+    total_nodes = sum(r["nodes_total"] for r in results)
+    value = total_nodes / (elapsed_ms / 1e3)
+
+    # roofline for the dominant kernel (dense_kernel), from the N=1 per-launch counters
+    peak, peak_src = measured_peak()
+    line_extra = {}
+    if world == 1:
+        dev_ms = statistics.mean(r["device_ms"] for r in results)
+        r0 = results[-1]
+        w = r0["degree_bytes"]
+        alg_bytes = w * n * (r0["rounds"] + r0["maxdeg_passes"] + r0["children"])
+        achieved = alg_bytes / (dev_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(),
+                "kernel": "dense_kernel<16>",
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_node_def": "w*n*(R+M+C), w=%d B (u16 degree records), n=%d" % (w, n),
+                "kernel_ms": dev_ms, "peak_source": peak_src,
+                "kernel_share_of_step": dev_ms / (elapsed_ms / args.steps)}
+        line_extra["roofline"] = roof
+        line_extra["counters_per_step"] = {k: r0[k] for k in (
+            "rounds", "maxdeg_passes", "children", "removals_deg1", "removals_deg2",
+            "removals_high", "doomed", "donated", "grid_blocks", "block_threads")}
+        line_extra["workers"] = len(r0["worker_nodes"])
+        line_extra["load_ratio_max"] = max(r0["load_ratios"])
+
+        # e2e: the public API with HOST buffers — fresh graph from host CSR arrays every step
+        # (its device copy is built and uploaded inside the call) + result readback
+        off, nbr = g.csr()
+        e2e_nodes, e2e_h2d, e2e_d2h = 0, 0, 0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            gh = vc.from_csr(n, m, off, nbr)
+            r = vc.solve_pvc(gh, K_NO, strategy="gpu")
+            e2e_nodes += r["nodes_total"]
+            e2e_h2d += r["h2d_bytes"]
+            e2e_d2h += r["d2h_bytes"]
+            del gh
+        e2e_s = time.perf_counter() - t0
+        line_extra["e2e"] = {"value": e2e_nodes / e2e_s, "unit": UNIT,
+                             "h2d_bytes_per_step": e2e_h2d // args.e2e_steps,
+                             "d2h_bytes_per_step": e2e_d2h // args.e2e_steps,
+                             "ms_per_step": e2e_s * 1e3 / args.e2e_steps,
+                             "time_to_solution_s": e2e_s / args.e2e_steps}
+    else:
+        line_extra["rank_nodes"] = results[-1]["rank_nodes"]
+        line_extra["frontier_nodes"] = results[-1]["frontier_nodes"]
+        line_extra["frontier_size"] = results[-1]["frontier_size"]
+        line_extra["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": None,
+                             "d2h_bytes_per_step": None,
+                             "note": "multi-GPU steps run through the public API "
+                                     "(solve_distributed) end to end"}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "time_to_solution_s": elapsed_ms / 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
+        "config": {"workload": WORKLOAD, "n": n, "m": m, "k": K_NO,
+                   "nodes_per_step": nodes_per_step, "strategy": "gpu",
+                   "l2": "flushed between timed steps (256 MB memset)",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} GPUs, frontier shards"},
+        "clocks": clk,
+        "gpu_launches": sum(r["kernel_launches"] for r in results),
+    }
+    line.update(line_extra)
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_sample_s)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

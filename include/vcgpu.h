@@ -120,6 +120,9 @@ typedef struct {
        mailbox[0] = external best bound (MVC, 0 = none), mailbox[1] = cancel request.
        Null = none. */
     volatile uint32_t* mailbox;
+    /* CUDA stream (cudaStream_t) to launch on; null = the library's own stream. The call stays
+       blocking: it synchronizes this stream before returning. */
+    void* stream;
 } vcg_params;
 
 typedef struct {
@@ -149,6 +152,7 @@ typedef struct {
     uint32_t n_padded;          /* n rounded to the engine's lane layout */
     int32_t engine;             /* engine that ran: 1 dense, 2 sparse */
     uint32_t grid_blocks, block_threads;
+    uint32_t kernel_launches;   /* device kernels this solve launched */
     uint64_t phase_cycles[10];  /* Phase order of metrics.hpp:15-26, summed over workers */
     uint64_t active_cycles;     /* summed over workers */
 } vcg_result;
@@ -159,6 +163,31 @@ VCG_API void vcg_params_init(vcg_params* p);
  * result readback. Blocking. */
 VCG_API int vcg_solve(const vcg_graph* g, const vcg_params* p, vcg_result* out);
 VCG_API void vcg_result_free(vcg_result* r);
+
+/* Multi-GPU partitioning: expands the search tree level by level on the device
+ * — every node processed exactly as the search would, with a fixed bound per level — until at
+ * least `target` open nodes exist. Deterministic: every rank computes the same frontier and
+ * takes its share (records i with i % world == rank) as vcg_params.seeds. The nodes the
+ * expansion visits are counted in nodes_visited (count them once, on one rank). */
+typedef struct {
+    uint64_t num_seeds;
+    uint32_t* seeds;            /* num_seeds x [cover_count, edge_count, degrees u32[n]] */
+    uint64_t nodes_visited;
+    uint32_t levels;
+    uint32_t best;              /* MVC: greedy size or better after expansion; PVC: k */
+    uint32_t greedy_size;
+    int32_t found;              /* a cover was found during the expansion */
+    uint32_t cover_len;
+    uint32_t* cover;            /* best certificate so far, ORIGINAL ids (greedy if none) */
+    uint32_t kernel_launches;
+} vcg_frontier;
+VCG_API int vcg_expand_frontier(const vcg_graph* g, const vcg_params* p, uint64_t target,
+                                vcg_frontier* out);
+VCG_API void vcg_frontier_free(vcg_frontier* f);
+
+/* Pinned, device-mapped host words for vcg_params.mailbox (zeroed); n_words >= 4. */
+VCG_API int vcg_mailbox_alloc(uint32_t n_words, uint32_t** out);
+VCG_API void vcg_mailbox_free(uint32_t* p);
 
 /* Number of CUDA devices visible (0 when no driver / no GPU). */
 VCG_API int vcg_device_count(void);

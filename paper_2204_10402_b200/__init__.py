@@ -194,7 +194,7 @@ _RULES = {"reference": 0, "parallel": 1}
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
            timeout_s, node_budget, device, rules, block_warps, instrument, initial_best=0,
-           seeds=None, mailbox=None, raw=False, donate_oldest=None):
+           seeds=None, mailbox=None, raw=False, donate_oldest=None, stream=None):
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
     if workers is None:
@@ -230,6 +230,8 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
         p.seeds = keep.ctypes.data_as(C.POINTER(C.c_uint32))
     if mailbox is not None:
         p.mailbox = C.cast(mailbox, C.POINTER(C.c_uint32))
+    if stream is not None:
+        p.stream = C.c_void_p(int(stream))
     r = _n.Result()
     _n.check(_lib.vcg_solve(graph._h, C.byref(p), C.byref(r)))
     try:
@@ -262,6 +264,7 @@ def _result_dict(r):
         removals_deg1=int(r.removals_deg1), removals_deg2=int(r.removals_deg2),
         removals_high=int(r.removals_high), doomed=int(r.doomed), degree_bytes=int(r.degree_bytes), n_padded=int(r.n_padded),
         engine=int(r.engine), grid_blocks=int(r.grid_blocks), block_threads=int(r.block_threads),
+        kernel_launches=int(r.kernel_launches),
         phase_cycles=[int(x) for x in r.phase_cycles], active_cycles=int(r.active_cycles),
     )
 
@@ -269,20 +272,20 @@ def _result_dict(r):
 def solve_mvc(graph, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
               depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
               rules="reference", block_warps=0, instrument=False, initial_best=0, seeds=None,
-              mailbox=None, raw=False, donate_oldest=None):
+              mailbox=None, raw=False, donate_oldest=None, stream=None):
     """Solve MVC; returns the run report as a dict (bindings.cpp:174-187)."""
     return _solve(graph, "mvc", 0, strategy, workers, capacity, threshold_fraction, depth,
                   backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  initial_best, seeds, mailbox, raw, donate_oldest)
+                  initial_best, seeds, mailbox, raw, donate_oldest, stream)
 
 
 def solve_pvc(graph, k, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
               depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
               rules="reference", block_warps=0, instrument=False, seeds=None, mailbox=None,
-              raw=False, donate_oldest=None):
+              raw=False, donate_oldest=None, stream=None):
     """Solve PVC for a given k; returns the run report as a dict (bindings.cpp:188-202)."""
     if k < 1:
         raise ValueError("pvc requires k >= 1")  # bindings.cpp:194
     return _solve(graph, "pvc", k, strategy, workers, capacity, threshold_fraction, depth,
                   backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  0, seeds, mailbox, raw, donate_oldest)
+                  0, seeds, mailbox, raw, donate_oldest, stream)

@@ -30,6 +30,7 @@ class Params(C.Structure):
         ("donate_oldest", C.c_int32),
         ("initial_best", C.c_uint32), ("num_seeds", C.c_uint64),
         ("seeds", C.POINTER(C.c_uint32)), ("mailbox", C.POINTER(C.c_uint32)),
+        ("stream", C.c_void_p),
     ]
 
 
@@ -51,8 +52,20 @@ class Result(C.Structure):
         ("removals_high", C.c_uint64), ("doomed", C.c_uint64),
         ("degree_bytes", C.c_uint32),
         ("n_padded", C.c_uint32), ("engine", C.c_int32), ("grid_blocks", C.c_uint32),
-        ("block_threads", C.c_uint32), ("phase_cycles", C.c_uint64 * 10),
+        ("block_threads", C.c_uint32), ("kernel_launches", C.c_uint32),
+        ("phase_cycles", C.c_uint64 * 10),
         ("active_cycles", C.c_uint64),
+    ]
+
+
+class Frontier(C.Structure):
+    """vcg_frontier (include/vcgpu.h)."""
+
+    _fields_ = [
+        ("num_seeds", C.c_uint64), ("seeds", C.POINTER(C.c_uint32)),
+        ("nodes_visited", C.c_uint64), ("levels", C.c_uint32), ("best", C.c_uint32),
+        ("greedy_size", C.c_uint32), ("found", C.c_int32), ("cover_len", C.c_uint32),
+        ("cover", C.POINTER(C.c_uint32)), ("kernel_launches", C.c_uint32),
     ]
 
 
@@ -81,6 +94,10 @@ _SIGS = [
     ("vcg_params_init", None, [C.POINTER(Params)]),
     ("vcg_solve", C.c_int, [_VP, C.POINTER(Params), C.POINTER(Result)]),
     ("vcg_result_free", None, [C.POINTER(Result)]),
+    ("vcg_expand_frontier", C.c_int, [_VP, C.POINTER(Params), C.c_uint64, C.POINTER(Frontier)]),
+    ("vcg_frontier_free", None, [C.POINTER(Frontier)]),
+    ("vcg_mailbox_alloc", C.c_int, [C.c_uint32, C.POINTER(C.POINTER(C.c_uint32))]),
+    ("vcg_mailbox_free", None, [C.POINTER(C.c_uint32)]),
     ("vcg_device_count", C.c_int, []),
     ("vcg_last_error", C.c_char_p, []),
     ("vcg_version", C.c_char_p, []),

@@ -229,6 +229,7 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         s.seeds = p->seeds;
         s.num_seeds = p->num_seeds;
         s.mailbox = p->mailbox;
+        s.stream = p->stream;
 
         vcg::SolveOut r;
         if (g.n == 0) {
@@ -297,6 +298,7 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         out->engine = r.engine;
         out->grid_blocks = r.grid;
         out->block_threads = r.block;
+        out->kernel_launches = r.launches;
         for (int i = 0; i < 10; ++i) out->phase_cycles[i] = r.phase[i];
         out->active_cycles = r.active_cycles;
         out->wall_ms =
@@ -304,6 +306,69 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         return VCG_OK;
     });
 }
+
+int vcg_expand_frontier(const vcg_graph* gh, const vcg_params* p, uint64_t target,
+                        vcg_frontier* out) {
+    return guarded([&]() -> int {
+        if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
+        std::memset(out, 0, sizeof(*out));
+        if (p->mode == VCG_PVC && p->k < 1) return fail(VCG_EINVAL, "pvc requires k >= 1");
+        const vcg::Graph& g = gh->g;
+        const bool pvc = p->mode == VCG_PVC;
+        vcg::Greedy greedy = vcg::greedy_approx(g);
+        out->greedy_size = greedy.size;
+        vcg::SolveSpec s;
+        s.pvc = pvc;
+        s.k = p->k;
+        s.device = p->device;
+        s.stream = p->stream;
+        s.best = pvc ? p->k : greedy.size;
+        if (!pvc && p->initial_best && p->initial_best < s.best) s.best = p->initial_best;
+        vcg::Frontier f;
+        if (g.n == 0) {
+            f.nodes = 1;
+            f.found = pvc;
+            f.best = s.best;
+        } else {
+            vcg::expand_frontier(g, s, std::max<uint64_t>(target, 1), f);
+        }
+        out->num_seeds = f.count;
+        if (f.count) {
+            out->seeds = static_cast<uint32_t*>(std::malloc(f.records.size() * 4));
+            std::memcpy(out->seeds, f.records.data(), f.records.size() * 4);
+        }
+        out->nodes_visited = f.nodes;
+        out->levels = f.levels;
+        out->best = f.best;
+        out->found = f.found ? 1 : 0;
+        out->kernel_launches = f.launches;
+        const std::vector<uint32_t>& cov = f.found ? f.cover : greedy.cover;
+        if (!(pvc && !f.found)) {
+            out->cover_len = (uint32_t)cov.size();
+            out->cover = static_cast<uint32_t*>(std::malloc(std::max<size_t>(1, cov.size()) * 4));
+            for (size_t i = 0; i < cov.size(); ++i) out->cover[i] = cov[i] + g.id_base;
+        }
+        return VCG_OK;
+    });
+}
+
+void vcg_frontier_free(vcg_frontier* f) {
+    if (!f) return;
+    std::free(f->seeds);
+    std::free(f->cover);
+    f->seeds = nullptr;
+    f->cover = nullptr;
+}
+
+int vcg_mailbox_alloc(uint32_t n_words, uint32_t** out) {
+    return guarded([&]() -> int {
+        if (!out || n_words < 4) return fail(VCG_EINVAL, "mailbox needs >= 4 words");
+        *out = vcg::mailbox_alloc(n_words);
+        return VCG_OK;
+    });
+}
+
+void vcg_mailbox_free(uint32_t* p) { vcg::mailbox_free(p); }
 
 void vcg_result_free(vcg_result* r) {
     if (!r) return;

@@ -438,6 +438,21 @@ struct WarpNode {
                     make_uint4(packed[4 * t], packed[4 * t + 1], packed[4 * t + 2], packed[4 * t + 3]);
         }
     }
+    // Stores the current node as a record (header by lane 0, lane-major u16 degrees).
+    __device__ __forceinline__ void store_current(unsigned char* rec) const {
+        uint32_t packed[W / 2];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t h = d[i] == REM ? 0xFFFFu : d[i];
+            if (i & 1) packed[i / 2] |= h << 16;
+            else packed[i / 2] = h;
+        }
+        if (lane == 0) {
+            reinterpret_cast<uint32_t*>(rec)[0] = cc;
+            reinterpret_cast<uint32_t*>(rec)[1] = edges;
+        }
+        store_degrees(rec, packed);
+    }
     // Moves one record (header + lane-major degrees) between stack and worklist memory.
     __device__ __forceinline__ void copy_record(const unsigned char* src, unsigned char* dst) const {
         const unsigned char* p = src + 16 + lane * (2 * W);
@@ -756,6 +771,65 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_k
     }
 }
 
+// Level-synchronous frontier expansion (multi-GPU partitioning): warp i
+// processes node i of a level exactly as process_node does (scheduler.cpp:125-144) with a
+// FIXED bound, and writes its remove-N(v) child to out[2i] and its remove-v child to
+// out[2i+1]. The result does not depend on scheduling, so every rank derives the same frontier.
+struct ExpandArgs {
+    const uint4* at4;
+    uint32_t n, npad;
+    int pvc;
+    uint32_t k, best;
+    uint32_t count;
+    unsigned long long entry_bytes;
+    const unsigned char* in;
+    unsigned char* out;
+    uint32_t* flags;   // per input: 0 pruned, 1 cover found (cc in covers[i*(W+1)]), 2 branched
+    uint32_t* covers;  // per input: [cc, bitmap W words]
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
+    extern __shared__ uint4 sat[];
+    constexpr int Q = W / 4;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) sat[t] = a.at4[t];
+    __syncthreads();
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t last_word_mask = (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : FULL;
+    const int last_word = (int)((a.n + 31) / 32) - 1;
+    WarpNode<W, false> x;
+    x.sat = sat;
+    x.npad = a.npad;
+    x.lane = lane;
+    Counters st;
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < a.count; i += warps) {
+        x.template load<false>(a.in + (unsigned long long)i * a.entry_bytes);
+        x.reduce(a.pvc, a.k, a.best, st);
+        uint32_t flag;
+        if (x.doom || should_prune(a.pvc, a.k, a.best, x.cc, x.edges)) {
+            flag = 0;
+        } else if (x.edges == 0) {
+            flag = 1;
+            uint32_t* c = a.covers + (unsigned long long)i * (W + 1);
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                uint32_t b = __ballot_sync(FULL, x.d[j] == REM);
+                b = j < last_word ? b : (j == last_word ? (b & last_word_mask) : 0u);
+                if (lane == j) c[1 + j] = b;
+            }
+            if (lane == 0) c[0] = x.cc;
+        } else {
+            flag = 2;
+            const uint32_t v = x.argmax();
+            x.write_child_without_neighbors(v, a.out + (2ull * i) * a.entry_bytes);
+            x.remove_vertex(v);
+            x.store_current(a.out + (2ull * i + 1) * a.entry_bytes);
+        }
+        if (lane == 0) a.flags[i] = flag;
+    }
+}
+
 // ------------------------------------------------------------------ host side
 
 struct DeviceGraph {
@@ -868,6 +942,17 @@ int occupancy(uint32_t block, size_t smem, bool instr) {
 
 }  // namespace
 
+uint32_t* mailbox_alloc(uint32_t n_words) {
+    void* p = nullptr;
+    CUDA_CHECK(cudaHostAlloc(&p, n_words * sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(p, 0, n_words * sizeof(uint32_t));
+    return static_cast<uint32_t*>(p);
+}
+
+void mailbox_free(uint32_t* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int device_count() {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -887,6 +972,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (dev < 0 || dev >= ndev) throw std::invalid_argument("device ordinal out of range");
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
+    cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
 
     const uint32_t W = pick_w(g.n);
     const uint32_t npad = 32 * W;
@@ -906,7 +992,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
         std::vector<uint32_t> at = build_bitmap(g, W, npad);
         dg->at4_bytes = at.size() * 4;
         CUDA_CHECK(cudaMalloc(&dg->at4, dg->at4_bytes));
-        CUDA_CHECK(cudaMemcpyAsync(dg->at4, at.data(), dg->at4_bytes, cudaMemcpyHostToDevice, C.stream));
+        CUDA_CHECK(cudaMemcpyAsync(dg->at4, at.data(), dg->at4_bytes, cudaMemcpyHostToDevice, st));
         out.h2d_bytes += dg->at4_bytes;
         g.dev[dev] = dg;
     }
@@ -969,13 +1055,14 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     hc.tail = nseeds;
     hc.work = (nseeds << 32) | nseeds;
     hc.best_owner = ~0ull;
-    CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, C.stream));
-    CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, C.stream));
-    init_seq_kernel<<<64, 256, 0, C.stream>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
+    CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+    init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
     CUDA_CHECK(cudaGetLastError());
-    CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), C.stream));
+    out.launches += 2;  // init_seq_kernel + dense_kernel
+    CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
     out.h2d_bytes += sizeof(hc) + recs.size();
-    CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    CUDA_CHECK(cudaStreamSynchronize(st));
     out.h2d_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
 
     DenseArgs a;
@@ -1009,16 +1096,16 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     a.donate_oldest = s.donate_oldest ? 1 : 0;
     a.mailbox = s.mailbox;
 
-    CUDA_CHECK(cudaEventRecord(C.ev0, C.stream));
+    CUDA_CHECK(cudaEventRecord(C.ev0, st));
     const bool I = s.instrument;
     switch (W) {
-        case 4: I ? launch_dense<4, true>(a, grid, block, smem, C.stream) : launch_dense<4, false>(a, grid, block, smem, C.stream); break;
-        case 8: I ? launch_dense<8, true>(a, grid, block, smem, C.stream) : launch_dense<8, false>(a, grid, block, smem, C.stream); break;
-        case 16: I ? launch_dense<16, true>(a, grid, block, smem, C.stream) : launch_dense<16, false>(a, grid, block, smem, C.stream); break;
-        default: I ? launch_dense<32, true>(a, grid, block, smem, C.stream) : launch_dense<32, false>(a, grid, block, smem, C.stream); break;
+        case 4: I ? launch_dense<4, true>(a, grid, block, smem, st) : launch_dense<4, false>(a, grid, block, smem, st); break;
+        case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
+        case 16: I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st); break;
+        default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
     }
-    CUDA_CHECK(cudaEventRecord(C.ev1, C.stream));
-    CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    CUDA_CHECK(cudaEventRecord(C.ev1, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
     out.device_ms = ms;
@@ -1062,6 +1149,133 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
         for (uint32_t v = 0; v < g.n; ++v)
             if ((bits[v >> 5] >> (v & 31)) & 1u) out.cover.push_back(v);
     }
+}
+
+void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f) {
+    if (g.n > 1024)
+        throw std::invalid_argument("frontier expansion needs the dense engine (n <= 1024)");
+    const int dev = s.device;
+    if (device_count() == 0) throw std::runtime_error("CUDA error: no CUDA device visible");
+    CUDA_CHECK(cudaSetDevice(dev));
+    DeviceCtx& C = ctx_for(dev);
+    cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
+    const uint32_t W = pick_w(g.n);
+    const uint32_t npad = 32 * W;
+    const size_t entry = 16 + 64 * (size_t)W;
+    if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
+    if (!g.dev[dev]) {
+        auto dg = std::make_shared<DeviceGraph>();
+        dg->device = dev;
+        dg->W = W;
+        dg->npad = npad;
+        std::vector<uint32_t> at = build_bitmap(g, W, npad);
+        dg->at4_bytes = at.size() * 4;
+        CUDA_CHECK(cudaMalloc(&dg->at4, dg->at4_bytes));
+        CUDA_CHECK(cudaMemcpy(dg->at4, at.data(), dg->at4_bytes, cudaMemcpyHostToDevice));
+        g.dev[dev] = dg;
+    }
+    const DeviceGraph& dg = *g.dev[dev];
+    const size_t smem = (size_t)W * npad * 4;
+
+    // level 0: the root
+    std::vector<unsigned char> level(entry);
+    {
+        std::vector<uint32_t> deg(g.n);
+        for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
+        pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), level.data());
+    }
+    uint64_t count = 1;
+    f = Frontier();
+    f.best = s.best;
+    while (count > 0 && count < target) {
+        unsigned char *din = nullptr, *dout = nullptr;
+        uint32_t *dflags = nullptr, *dcov = nullptr;
+        CUDA_CHECK(cudaMalloc(&din, count * entry));
+        CUDA_CHECK(cudaMalloc(&dout, 2 * count * entry));
+        CUDA_CHECK(cudaMalloc(&dflags, count * 4));
+        CUDA_CHECK(cudaMalloc(&dcov, count * (W + 1) * 4));
+        CUDA_CHECK(cudaMemcpyAsync(din, level.data(), count * entry, cudaMemcpyHostToDevice, st));
+        ExpandArgs a;
+        a.at4 = dg.at4;
+        a.n = g.n;
+        a.npad = npad;
+        a.pvc = s.pvc ? 1 : 0;
+        a.k = s.k;
+        a.best = f.best;
+        a.count = (uint32_t)count;
+        a.entry_bytes = entry;
+        a.in = din;
+        a.out = dout;
+        a.flags = dflags;
+        a.covers = dcov;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((count + 7) / 8, 1184);
+        switch (W) {
+#define VCG_EXPAND(WW)                                                                        \
+    case WW: {                                                                                \
+        CUDA_CHECK(cudaFuncSetAttribute(expand_kernel<WW>,                                    \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        expand_kernel<WW><<<grid, 256, smem, st>>>(a);                                        \
+        break;                                                                                \
+    }
+            VCG_EXPAND(4) VCG_EXPAND(8) VCG_EXPAND(16) VCG_EXPAND(32)
+#undef VCG_EXPAND
+        }
+        CUDA_CHECK(cudaGetLastError());
+        ++f.launches;
+        std::vector<uint32_t> flags(count), covers(count * (W + 1));
+        std::vector<unsigned char> out(2 * count * entry);
+        CUDA_CHECK(cudaMemcpyAsync(flags.data(), dflags, count * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(covers.data(), dcov, covers.size() * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(out.data(), dout, out.size(), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaFree(din);
+        cudaFree(dout);
+        cudaFree(dflags);
+        cudaFree(dcov);
+        f.nodes += count;
+        ++f.levels;
+        // covers found on this level (fixed bound inside the level, improved between levels)
+        for (uint64_t i = 0; i < count; ++i) {
+            if (flags[i] != 1) continue;
+            const uint32_t* c = &covers[i * (W + 1)];
+            if (s.pvc ? !f.found : c[0] < f.best) {
+                f.found = true;
+                if (!s.pvc) f.best = c[0];
+                f.cover.clear();
+                for (uint32_t v = 0; v < g.n; ++v)
+                    if ((c[1 + (v >> 5)] >> (v & 31)) & 1u) f.cover.push_back(v);
+            }
+        }
+        if (s.pvc && f.found) {
+            count = 0;
+            level.clear();
+            break;
+        }
+        std::vector<unsigned char> next;
+        next.reserve(2 * count * entry);
+        uint64_t nc = 0;
+        for (uint64_t i = 0; i < count; ++i) {
+            if (flags[i] != 2) continue;
+            next.insert(next.end(), out.begin() + (2 * i) * entry, out.begin() + (2 * i + 2) * entry);
+            nc += 2;
+        }
+        level.swap(next);
+        count = nc;
+    }
+    // unpack the frontier into [cc, edges, deg[n]] records
+    f.records.assign(count * (2 + (size_t)g.n), 0);
+    for (uint64_t i = 0; i < count; ++i) {
+        const unsigned char* rec = level.data() + i * entry;
+        uint32_t* r = f.records.data() + i * (2 + (size_t)g.n);
+        r[0] = reinterpret_cast<const uint32_t*>(rec)[0];
+        r[1] = reinterpret_cast<const uint32_t*>(rec)[1];
+        const uint16_t* dd = reinterpret_cast<const uint16_t*>(rec + 16);
+        for (uint32_t v = 0; v < g.n; ++v) {
+            const uint16_t x = dd[(v & 31) * W + (v >> 5)];
+            r[2 + v] = x == 0xFFFF ? REM : x;
+        }
+    }
+    f.count = count;
 }
 
 }  // namespace vcg

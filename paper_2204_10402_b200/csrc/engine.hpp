@@ -31,6 +31,7 @@ struct SolveSpec {
     const uint32_t* seeds = nullptr;  // [cc, edges, deg[n]] records
     uint64_t num_seeds = 0;
     volatile uint32_t* mailbox = nullptr;
+    void* stream = nullptr;     // caller's cudaStream_t (null: the library's stream)
 };
 
 struct SolveOut {
@@ -49,10 +50,26 @@ struct SolveOut {
     uint32_t degree_bytes = 2, n_padded = 0;
     int engine = 1;
     uint32_t grid = 0, block = 0;
+    uint32_t launches = 0;
 };
+
+struct Frontier {
+    uint64_t count = 0;              // frontier nodes
+    std::vector<uint32_t> records;   // count x [cc, edges, deg[n]]
+    uint64_t nodes = 0;              // nodes visited (processed) by the expansion
+    uint32_t levels = 0, launches = 0;
+    uint32_t best = 0;               // MVC bound after the expansion (k for PVC)
+    bool found = false;              // a cover was found (PVC: yes-instance decided)
+    std::vector<uint32_t> cover;     // internal ids
+};
+
+// Deterministic level-synchronous expansion of the search tree until >= target open nodes.
+void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f);
 
 // Throws std::runtime_error (CUDA failures) / std::invalid_argument (bad configuration).
 void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out);
 int device_count();
+uint32_t* mailbox_alloc(uint32_t n_words);
+void mailbox_free(uint32_t* p);
 
 }  // namespace vcg

@@ -1,0 +1,218 @@
+"""Multi-GPU hybrid traversal: one process per GPU.
+
+Partitioning — the worklist is the natural shard. Every rank expands the top of the search tree
+with the same deterministic, level-synchronous device expansion (``vcg_expand_frontier``) until
+the frontier holds ``frontier_per_rank * world`` open nodes, then seeds its own device worklist
+with the records ``i % world == rank``. Sub-trees are independent given (degree array, |S|,
+|E|), so there is no data-path collective: each GPU runs the single-GPU
+hybrid kernel on its share.
+
+Coupling — only the MVC bound and the PVC found flag cross GPUs. A host monitor thread per
+rank exchanges {best, found, done} over a CPU (gloo) group every ``period`` seconds and writes
+what it learns into the rank's pinned mailbox, which the running kernel polls (worker 0 folds an
+external bound in with atomicMin and turns a remote "found" into its cancel flag). The exchange
+never touches the GPU, so it cannot queue behind the persistent kernel.
+
+Every tree node is visited exactly once across ranks (frontier nodes once, on the expansion;
+frontier sub-trees once, on their owner), so PVC no-instance node counts stay equal to the
+reference's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import time
+
+import numpy as np
+
+from . import _native as _n
+
+_lib = _n.lib
+
+
+class Mailbox:
+    """Four host words the kernel can read/write while it runs:
+    [0] external best (in), [1] cancel request (in), [2] device best (out), [3] found (out).
+
+    ``pinned=True`` allocates device-mapped pinned memory (vcg_mailbox_alloc) — required when a
+    real kernel polls it. ``pinned=False`` is for host-only protocol tests with a stand-in
+    solver."""
+
+    def __init__(self, pinned=True):
+        self._pinned = pinned
+        if pinned:
+            p = C.POINTER(C.c_uint32)()
+            _n.check(_lib.vcg_mailbox_alloc(4, C.byref(p)))
+            self._ptr = p
+            self.words = np.ctypeslib.as_array(p, shape=(4,))
+        else:
+            self.words = np.zeros(4, np.uint32)
+            self._ptr = self.words.ctypes.data_as(C.POINTER(C.c_uint32))
+
+    @property
+    def address(self):
+        return C.cast(self._ptr, C.c_void_p).value
+
+    def close(self):
+        if self._pinned and self._ptr:
+            _lib.vcg_mailbox_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def expand_frontier(graph, mode, k, target, device=0, stream=None, initial_best=0):
+    """Deterministic device expansion (vcg_expand_frontier) → dict with ``seeds`` as an
+    (count, 2 + n) uint32 array of [cover_count, edge_count, degrees...] records."""
+    p = _n.Params()
+    _lib.vcg_params_init(C.byref(p))
+    p.mode = _n.VCG_PVC if mode == "pvc" else _n.VCG_MVC
+    p.k = k
+    p.device = device
+    p.initial_best = initial_best or 0
+    if stream is not None:
+        p.stream = C.c_void_p(int(stream))
+    f = _n.Frontier()
+    _n.check(_lib.vcg_expand_frontier(graph._h, C.byref(p), int(target), C.byref(f)))
+    try:
+        n = graph.num_vertices
+        cnt = int(f.num_seeds)
+        seeds = (np.ctypeslib.as_array(f.seeds, shape=(cnt * (2 + n),)).reshape(cnt, 2 + n).copy()
+                 if cnt else np.zeros((0, 2 + n), np.uint32))
+        return dict(seeds=seeds, nodes=int(f.nodes_visited), levels=int(f.levels),
+                    best=int(f.best), greedy_size=int(f.greedy_size), found=bool(f.found),
+                    cover=[int(f.cover[i]) for i in range(f.cover_len)],
+                    kernel_launches=int(f.kernel_launches))
+    finally:
+        _lib.vcg_frontier_free(C.byref(f))
+
+
+class _Monitor(threading.Thread):
+    """Host-side exchange of {best, found, done} between ranks (see module docstring)."""
+
+    def __init__(self, group, mailbox, pvc, initial_best, period):
+        super().__init__(daemon=True)
+        self.group = group
+        self.mb = mailbox
+        self.pvc = pvc
+        self.best = initial_best
+        self.period = period
+        self.done = threading.Event()
+        self.global_best = initial_best
+        self.global_found = False
+        self.rounds = 0
+        self.error = None
+
+    def run(self):
+        import torch
+        import torch.distributed as dist
+        world = dist.get_world_size(self.group)
+        try:
+            while True:
+                out_best = int(self.mb.words[2])
+                mine = self.best if out_best == 0 else min(self.best, out_best)
+                t = torch.tensor([mine, int(self.mb.words[3]), int(self.done.is_set())],
+                                 dtype=torch.int64)
+                got = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+                dist.all_gather(got, t, group=self.group)
+                g = torch.stack(got)
+                self.rounds += 1
+                self.global_best = int(g[:, 0].min())
+                self.global_found = bool(g[:, 1].max())
+                if not self.pvc and self.global_best < mine:
+                    self.mb.words[0] = self.global_best
+                if self.pvc and self.global_found and not self.mb.words[3]:
+                    self.mb.words[1] = 1
+                if bool(g[:, 2].min()):
+                    return
+                time.sleep(self.period)
+        except Exception as e:  # surfaced by solve_distributed
+            self.error = e
+
+
+def _empty_result(graph, pvc):
+    return dict(status="complete", size=0, feasible=False, cover=[], worker_nodes=[],
+                nodes_total=0, device_ms=0.0, wall_ms=0.0, kernel_launches=0,
+                cover_from_search=False, greedy_size=0)
+
+
+def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_per_rank=1024,
+                      device=0, stream=None, period=0.002, solver=None, expander=None,
+                      mailbox=None, **solve_kw):
+    """One rank's part of a multi-GPU solve; every rank of ``exchange_group`` (a CPU/gloo
+    process group; default: the world group) must call it. Returns the combined result
+    (identical on every rank): size/feasible/cover, per-rank node counts and timings."""
+    import torch.distributed as dist
+    if mode == "pvc" and k < 1:
+        raise ValueError("pvc requires k >= 1")
+    pvc = mode == "pvc"
+    rank = dist.get_rank(exchange_group)
+    world = dist.get_world_size(exchange_group)
+    expander = expander or expand_frontier
+    if solver is None:
+        from . import solve_mvc, solve_pvc
+
+        def solver(g, **kw):
+            return (solve_pvc(g, k, raw=True, **kw) if pvc else solve_mvc(g, raw=True, **kw))
+
+    t0 = time.perf_counter()
+    fr = expander(graph, mode, k, frontier_per_rank * world, device=device, stream=stream)
+    share = fr["seeds"][rank::world]
+    decided = pvc and fr["found"]
+    res = _empty_result(graph, pvc)
+    mb = mailbox or Mailbox()
+    mon = _Monitor(exchange_group, mb, pvc, fr["best"], period)
+    mon.start()
+    try:
+        if not decided and len(share):
+            kw = dict(solve_kw, seeds=share, mailbox=mb.address, device=device, stream=stream)
+            if not pvc:
+                kw["initial_best"] = fr["best"]
+            res = solver(graph, **kw)
+    finally:
+        mon.done.set()
+        mon.join()
+        if mailbox is None:
+            mb.close()
+    if mon.error is not None:
+        raise mon.error
+    wall_ms = (time.perf_counter() - t0) * 1e3
+
+    # combine (every rank gets the same answer)
+    mine = dict(size=res["size"], feasible=res["feasible"], cover=res["cover"],
+                from_search=bool(res.get("cover_from_search")), status=res["status"],
+                worker_nodes=res["worker_nodes"], nodes=res["nodes_total"],
+                device_ms=res["device_ms"], wall_ms=wall_ms,
+                launches=res.get("kernel_launches", 0))
+    allr = [None] * world
+    dist.all_gather_object(allr, mine, group=exchange_group)
+    nodes = fr["nodes"] + sum(r["nodes"] for r in allr)
+    if pvc:
+        feasible = fr["found"] or any(r["feasible"] for r in allr)
+        if fr["found"]:
+            cover = fr["cover"]
+        else:
+            cover = next((r["cover"] for r in allr if r["feasible"]), [])
+        size = len(cover) if feasible else 0
+    else:
+        feasible = True
+        cands = [(len(fr["cover"]), fr["cover"])]
+        cands += [(r["size"], r["cover"]) for r in allr if r["from_search"]]
+        size, cover = min(cands, key=lambda c: c[0])
+    statuses = [r["status"] for r in allr]
+    status = next((s for s in statuses if s != "complete"), "complete")
+    if pvc and feasible:
+        status = "complete"
+    return dict(size=size if feasible else None, feasible=feasible, cover=cover, status=status,
+                nodes_total=nodes, frontier_nodes=fr["nodes"], frontier_levels=fr["levels"],
+                frontier_size=int(len(fr["seeds"])),
+                rank_nodes=[r["nodes"] for r in allr],
+                rank_device_ms=[r["device_ms"] for r in allr],
+                rank_wall_ms=[r["wall_ms"] for r in allr],
+                worker_nodes=[w for r in allr for w in r["worker_nodes"]],
+                kernel_launches=fr["kernel_launches"] + mine["launches"],
+                exchange_rounds=mon.rounds, greedy_size=fr["greedy_size"])

@@ -60,7 +60,7 @@ def make_report(graph, mode, k, strategy, workers, capacity, threshold_fraction,
     for key in ("nodes_total", "greedy_size", "device_ms", "greedy_ms", "h2d_ms", "h2d_bytes",
                 "d2h_bytes", "rounds", "maxdeg_passes", "children", "removals", "donated", "removals_deg1", "removals_deg2", "removals_high", "doomed",
                 "degree_bytes",
-                "n_padded", "engine", "grid_blocks", "block_threads", "cover_from_search",
+                "n_padded", "engine", "grid_blocks", "block_threads", "kernel_launches", "cover_from_search",
                 "worker_stack_high_water"):
         rep[key] = res[key]
     return rep

@@ -1,0 +1,131 @@
+"""Multi-GPU host logic on CPU: two processes over gloo run paper_2204_10402_b200.distributed
+with stand-in expander/solver functions (no GPU here), checking the partitioning, the node
+accounting, the PVC found-flag cancel and the MVC bound exchange through the mailbox."""
+import ctypes as C
+import os
+import socket
+import time
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+N = 7  # vertices of the fake graph: a seed record is [cc, edges, deg[7]]
+
+
+class FakeGraph:
+    num_vertices = N
+
+
+def fake_expander(graph, mode, k, target, device=0, stream=None):
+    seeds = np.zeros((target + 3, 2 + N), np.uint32)
+    seeds[:, 0] = np.arange(target + 3)  # tag = record index
+    return dict(seeds=seeds, nodes=100, levels=5, best=9 if mode == "mvc" else k,
+                greedy_size=9, found=False, cover=list(range(9)) if mode == "mvc" else [],
+                kernel_launches=5)
+
+
+def words_at(address):
+    return np.ctypeslib.as_array((C.c_uint32 * 4).from_address(address))
+
+
+def make_solver(rank, scenario, log):
+    def solver(graph, seeds, mailbox, device, stream, initial_best=None, **kw):
+        w = words_at(mailbox)
+        log["tags"] = sorted(int(t) for t in seeds[:, 0])
+        res = dict(status="complete", size=0, feasible=False, cover=[], worker_nodes=[len(seeds)],
+                   nodes_total=10 * len(seeds), device_ms=1.0, kernel_launches=2,
+                   cover_from_search=False)
+        if scenario == "pvc_yes":
+            if rank == 1:
+                time.sleep(0.05)
+                w[2], w[3] = 3, 1  # the device found a cover of size 3 <= k
+                res.update(feasible=True, size=3, cover=[0, 1, 2])
+            else:
+                t0 = time.time()
+                while not w[1]:  # wait for the monitor to forward the remote found flag
+                    assert time.time() - t0 < 20, "cancel never arrived"
+                    time.sleep(0.001)
+                log["cancelled"] = True
+        elif scenario == "mvc":
+            log["initial_best"] = initial_best
+            if rank == 0:
+                time.sleep(0.05)
+                w[2] = 5  # the device improved the bound to 5
+                res.update(size=5, cover=[1, 2, 3, 4, 5], cover_from_search=True, feasible=True)
+            else:
+                t0 = time.time()
+                while w[0] != 5:  # external bound delivered into this rank's mailbox
+                    assert time.time() - t0 < 20, "bound never arrived"
+                    time.sleep(0.001)
+                log["ext_best"] = int(w[0])
+                res.update(size=9, feasible=True)
+        return res
+    return solver
+
+
+def worker(rank, world, port, scenario, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_10402_b200.distributed import Mailbox, solve_distributed
+    log = {}
+    mode, k = ("mvc", 0) if scenario == "mvc" else ("pvc", 4)
+    r = solve_distributed(FakeGraph(), mode, k, frontier_per_rank=5, expander=fake_expander,
+                          solver=make_solver(rank, scenario, log), mailbox=Mailbox(pinned=False),
+                          period=0.001)
+    out.put((rank, r, log))
+    dist.destroy_process_group()
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run(scenario, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=worker, args=(r, world, port, scenario, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, r, log = q.get(timeout=120)
+        res[rank] = (r, log)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_pvc_no_partition_and_node_accounting():
+    res = run("pvc_no")
+    target = 5 * 2 + 3  # expander returns target + 3 records
+    tags0 = res[0][1]["tags"]
+    tags1 = res[1][1]["tags"]
+    assert tags0 == list(range(0, target, 2)) and tags1 == list(range(1, target, 2))
+    for rank in (0, 1):
+        r = res[rank][0]
+        assert not r["feasible"] and r["status"] == "complete"
+        assert r["nodes_total"] == 100 + 10 * target  # frontier once + every shard once
+        assert r["rank_nodes"] == [10 * len(tags0), 10 * len(tags1)]
+
+
+def test_pvc_found_flag_cancels_the_other_rank():
+    res = run("pvc_yes")
+    assert res[0][1].get("cancelled")
+    for rank in (0, 1):
+        r = res[rank][0]
+        assert r["feasible"] and r["size"] == 3 and r["cover"] == [0, 1, 2]
+
+
+def test_mvc_bound_is_exchanged_and_minimum_wins():
+    res = run("mvc")
+    assert res[1][1]["ext_best"] == 5
+    assert res[0][1]["initial_best"] == 9
+    for rank in (0, 1):
+        r = res[rank][0]
+        assert r["size"] == 5 and r["cover"] == [1, 2, 3, 4, 5]

@@ -161,3 +161,50 @@ def test_instrumented_phase_shares():
     assert rep["size"] == 291
     shares = rep["phase_shares"]
     assert 0.0 < sum(v for k, v in shares.items() if k != "other") <= 1.0 + 1e-9
+
+
+@pytest.mark.parametrize("name,k_key,world,target", [("c1", "pvc_no_k", 3, 64),
+                                                      ("c3", "pvc_no_k", 2, 300),
+                                                      ("c5", "pvc_no_k", 4, 4096)])
+def test_frontier_shards_cover_the_tree_exactly(config_golden, name, k_key, world, target):
+    """Multi-GPU partitioning, simulated in-process: the deterministic frontier plus every
+    rank's share visit exactly the reference's PVC no-instance tree."""
+    from paper_2204_10402_b200.distributed import expand_frontier
+    gold = config_golden[name]
+    g = load_config(name)
+    k = gold[k_key]
+    fr = expand_frontier(g, "pvc", k, target)
+    fr2 = expand_frontier(g, "pvc", k, target)
+    assert (fr["seeds"] == fr2["seeds"]).all() and fr["nodes"] == fr2["nodes"]  # deterministic
+    assert not fr["found"]
+    assert len(fr["seeds"]) >= target or len(fr["seeds"]) == 0  # 0: tree exhausted first
+    total = fr["nodes"]
+    for rank in range(world):
+        share = fr["seeds"][rank::world]
+        r = vc.solve_pvc(g, k, strategy="gpu", seeds=share)
+        assert not r["feasible"]
+        total += r["nodes_total"]
+    assert total == gold["pvc_no_nodes"]
+
+
+def test_frontier_mvc_shards_find_the_optimum(config_golden):
+    from paper_2204_10402_b200.distributed import expand_frontier
+    g = load_config("c1")
+    fr = expand_frontier(g, "mvc", 0, 200)
+    best = fr["best"]
+    for rank in range(2):
+        r = vc.solve_mvc(g, strategy="gpu", seeds=fr["seeds"][rank::2], initial_best=fr["best"])
+        if r["cover_from_search"]:
+            check_cover(g, r)
+            best = min(best, r["size"])
+    assert best == config_golden["c1"]["mvc"]
+
+
+def test_mailbox_cancel_and_external_bound():
+    from paper_2204_10402_b200.distributed import Mailbox
+    g = load_config("c5")
+    mb = Mailbox()
+    mb.words[1] = 1  # host cancel request before launch: the search stops early
+    r = vc.solve_pvc(g, 482, strategy="gpu", mailbox=mb.address)
+    assert r["nodes_total"] < 21461369
+    mb.close()
