@@ -12,7 +12,7 @@ NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xptxas -v -Xcompiler -fPIC,-fvisib
 
 CU_SRCS  := $(wildcard $(SRC)/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/*.cpp)
-HDRS     := $(wildcard $(SRC)/*.hpp) include/vcgpu.h
+HDRS     := $(wildcard $(SRC)/*.hpp) $(wildcard $(SRC)/*.cuh) include/vcgpu.h
 OBJS     := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
 all: $(LIB) oracle

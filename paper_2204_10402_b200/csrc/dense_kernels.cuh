@@ -1,0 +1,766 @@
+// dense_kernels.cuh — device code of the dense engine (n <= 1024): the warp-per-node hybrid
+// traversal kernel and the level-synchronous frontier expansion kernel.
+//
+// Reference path replaced: run_hybrid (proj/src/scheduler.cpp:328-359) — hybrid_worker
+// (:146-212), process_node (:125-144) — reduce_to_fixpoint and the three rule passes
+// (reductions.cpp:7-104), should_prune (bounds.cpp:21-30), max_degree_vertex and
+// remove_*_into_cover (search_node.cpp:16-46), GlobalWorklist (worklist.cpp:11-48).
+//
+// Layout:
+//  * one WARP = one worker; the current node's degree array lives in REGISTERS: lane l holds
+//    the degrees of vertices 32*i + l (i < W), u32, kRemoved = 0xFFFFFFFF;
+//  * the read-only graph is an adjacency bitmap staged once per CTA in shared memory, word j of
+//    vertex w's row at uint4 group (j/4)*npad + w (column-coalesced, row-broadcast);
+//  * deferred nodes are 16 + 64*W byte records: {cover_count, edge_count, 0, 0} then lane-major
+//    u16 degrees (lane l's W entries contiguous), in a per-warp stack in HBM or the device ring.
+//
+// Instruction footprint matters more than instruction count here: with the rule code inlined
+// at every call site the W=16 kernel was 128 KB of SASS and 64% of warp stalls were
+// `no_instruction`. Every primitive below therefore has ONE call site in the node loop
+// (remove_vertex: two), the three rule passes share one rolled loop with a range predicate, and
+// loops that do not index the register array are not unrolled.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace vcg {
+
+constexpr uint32_t REM = 0xFFFFFFFFu;
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr unsigned long long ONE_PENDING = 1ull << 32;
+
+// ------------------------------------------------------------------ device-global state
+
+struct Ctl {
+    // line 0: read by every worker once per node (one vector load + one scalar load)
+    uint32_t best;    // MVC bound (atomicMin); PVC: k
+    uint32_t cancel;  // 1 = stop: PVC found, timeout, budget, host request
+    uint32_t found;   // PVC: a cover of size <= k was recorded
+    uint32_t pad0;
+    // (pending << 32) | size: pending = queued items + active workers (termination at 0);
+    // size = queued items + in-flight enqueue reservations (threshold gate, capacity)
+    unsigned long long work;
+    unsigned long long pad1;
+    uint32_t pad2[24];
+    // line 1: ring tickets (per-slot sequence numbers publish / free each slot)
+    unsigned long long head, tail;
+    uint32_t pad3[28];
+    // line 2: results
+    unsigned long long nodes_total, best_owner;
+    int32_t status;
+    uint32_t pad4[27];
+};
+static_assert(sizeof(Ctl) == 384, "Ctl layout");
+
+struct WStats {
+    unsigned long long nodes, rounds, maxdeg, children, rm1, rm2, rmh, high_water, donated,
+        active, max_queue, dooms;
+    unsigned long long phase[10];
+};
+
+enum Phase { PH_WL_REMOVE, PH_WL_ADD, PH_STACK, PH_DEG1, PH_DEG2, PH_HIGH, PH_MAXDEG,
+             PH_BRANCH_NBRS, PH_BRANCH_V, PH_PRUNE };  // metrics.hpp:15-26 order
+
+struct DenseArgs {
+    const uint4* at4;         // adjacency bitmap, [W/4][npad] uint4 groups
+    uint32_t n, npad, m;
+    int pvc;
+    uint32_t k;
+    uint32_t capacity;        // logical worklist capacity (try_add rejects at capacity)
+    uint32_t ring_mask;       // ring slots - 1 (power of two >= max(capacity, 2))
+    uint32_t threshold;
+    uint32_t workers;
+    uint32_t stack_bound;
+    unsigned long long entry_bytes;
+    unsigned char* stacks;    // workers * stack_bound * entry_bytes
+    unsigned char* wl;        // ring slots * entry_bytes
+    unsigned long long* seq;  // ring slots
+    Ctl* ctl;
+    uint32_t* cover_slots;    // workers * W words
+    WStats* stats;
+    unsigned long long node_budget;
+    unsigned long long timeout_ns;
+    unsigned long long flush_every;  // visits between node-counter flushes / limit checks
+    uint32_t backoff_ns;
+    int seq_mode;             // never donate (solve_*_seq semantics)
+    int donate_oldest;        // donate the bottom (oldest) stacked node instead of the new child
+    volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out,
+                                 // [3] found out
+};
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t comp(const uint4& r, int c) {
+    return c == 0 ? r.x : c == 1 ? r.y : c == 2 ? r.z : r.w;
+}
+
+// ReductionBound::current (reductions.hpp:19-27)
+__device__ __forceinline__ uint32_t limit_for(int pvc, uint32_t k, uint32_t best, uint32_t cc) {
+    if (pvc) return cc >= k ? 0u : k - cc;
+    const uint32_t spend = cc + 1;
+    return best <= spend ? 0u : best - spend;
+}
+// should_prune (bounds.cpp:21-30)
+__device__ __forceinline__ bool should_prune(int pvc, uint32_t k, uint32_t best, uint32_t cc,
+                                             uint32_t edges) {
+    if (pvc) {
+        if (cc > k) return true;
+        const unsigned long long s = k - cc;
+        return (unsigned long long)edges > s * s;
+    }
+    if (cc >= best) return true;
+    const unsigned long long s = best - cc - 1;
+    return (unsigned long long)edges > s * s;
+}
+
+// Host mailbox (pinned, mapped): one poller per device (worker 0) folds an external MVC bound
+// into the device bound and turns a host cancel request into the device cancel flag.
+__device__ __noinline__ void poll_mailbox(volatile uint32_t* mb, int pvc, Ctl* ctl) {
+    const uint32_t eb = mb[0];
+    if (!pvc && eb) atomicMin(&ctl->best, eb);
+    if (mb[1]) atomicExch(&ctl->cancel, 1u);
+}
+
+struct Counters {
+    unsigned long long nodes = 0, rounds = 0, maxdeg = 0, children = 0, rm1 = 0, rm2 = 0,
+                       rmh = 0, high_water = 0, donated = 0, max_queue = 0, dooms = 0;
+    unsigned long long phase[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+// ------------------------------------------------------------------ one search node per warp
+
+template <int W, bool INSTR>
+struct WarpNode {
+    static constexpr int Q = W / 4;  // uint4 groups per bitmap row
+    uint32_t d[W];                   // degree of vertex 32*i + lane (meaningless once removed)
+    uint32_t alv;                    // bit i: vertex 32*i + lane is alive (not in the cover)
+    uint32_t aw;                     // lane j < W: alive bitmap word j (vertices 32j..32j+31)
+    uint32_t cc, edges;              // uniform
+    bool doom;                       // uniform: proven to be pruned (see reduce)
+    const uint4* sat;                // shared adjacency bitmap
+    uint4* sx;                       // per-warp shared scratch: the branch mask, W words
+    uint32_t* ss;                    // per-warp shared scratch: W x 32 partial degrees
+    uint32_t npad;
+    int lane;
+
+    __device__ __forceinline__ bool alive(int i) const { return (alv >> i) & 1u; }
+    __device__ __forceinline__ uint32_t row_word(uint32_t u, uint32_t j) const {
+        return reinterpret_cast<const uint32_t*>(sat)[((j >> 2) * npad + u) * 4 + (j & 3)];
+    }
+    __device__ __forceinline__ void rebuild_aw() {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t b = __ballot_sync(FULL, alive(i));
+            if (lane == i) aw = b;
+        }
+    }
+    // search_node.cpp:16-25 remove_vertex_into_cover(u), u alive: its degree is the popcount of
+    // its alive row; one broadcast row load per 4 words decrements every neighbour.
+    __device__ __forceinline__ void remove_vertex(uint32_t u) {
+        uint32_t du = lane < W ? __popc(row_word(u, lane) & aw) : 0u;
+        du = __reduce_add_sync(FULL, du);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint4 r = sat[q * npad + u];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) d[4 * q + c] -= (comp(r, c) >> lane) & 1u;
+        }
+        if (lane == (int)(u & 31)) alv &= ~(1u << (u >> 5));
+        if (lane == (int)(u >> 5)) aw &= ~(1u << (u & 31));
+        cc += 1;
+        edges -= du;
+    }
+    // First alive vertex v >= pos with lo <= d[v] <= hi at this moment — exactly the next vertex
+    // the reference's ascending pass would act on. -1 if none.
+    // Bit-sliced: each lane builds the mask of its own candidates (bit i = vertex 32*i + lane),
+    // and one REDUX picks the smallest id — no per-word ballots, no branches.
+    __device__ __forceinline__ uint32_t range_mask(uint32_t lo, uint32_t hi) const {
+        const uint32_t span = hi - lo;
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) m |= (d[i] - lo <= span ? 1u : 0u) << i;
+        return m & alv;
+    }
+    __device__ __forceinline__ int find_first(int pos, uint32_t lo, uint32_t hi) const {
+        const uint32_t pi = (uint32_t)pos >> 5;
+        uint32_t m = range_mask(lo, hi);
+        m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
+        const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
+        const uint32_t v = __reduce_min_sync(FULL, key);
+        return v == FULL ? -1 : (int)v;
+    }
+    // The first two alive neighbours of v in id order (= CSR order; the second is -1 if absent).
+    __device__ __forceinline__ void first_neighbors(uint32_t v, int& p0, int& p1) const {
+        const uint32_t xl = lane < W ? (row_word(v, lane) & aw) : 0u;
+        const uint32_t b = __ballot_sync(FULL, xl != 0);
+        const int j0 = __ffs(b) - 1;
+        const uint32_t w0 = __shfl_sync(FULL, xl, j0 & 31);
+        p0 = 32 * j0 + __ffs(w0) - 1;
+        const uint32_t w0b = w0 & (w0 - 1);
+        const uint32_t b2 = b & ~(1u << j0);
+        const int j1 = w0b ? j0 : __ffs(b2) - 1;
+        const uint32_t w1 = w0b ? w0b : __shfl_sync(FULL, xl, j1 & 31);
+        p1 = (w0b || b2) ? 32 * j1 + __ffs(w1) - 1 : -1;
+    }
+    // Number of alive vertices of degree > lim (degree > lim >= 0 implies degree > 0).
+    __device__ __forceinline__ uint32_t count_above(uint32_t lim) const {
+        return __reduce_add_sync(FULL, __popc(range_mask(lim + 1u, 0xFFFFu)));
+    }
+    // Can any rule fire? (an alive vertex of degree 1 or 2, or one above the limit)
+    __device__ __forceinline__ bool any_candidate(uint32_t lim) const {
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) m |= (d[i] - 1u <= 1u || d[i] > lim ? 1u : 0u) << i;
+        return __any_sync(FULL, (m & alv) != 0);
+    }
+    // search_node.cpp:34-46: smallest id among alive vertices of maximum degree
+    __device__ __forceinline__ uint32_t argmax() const {
+        uint32_t mx = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            mx = max(mx, alive(i) ? ((d[i] << 11) | (2047u - (32u * i + lane))) : 0u);
+        mx = __reduce_max_sync(FULL, mx);
+        return 2047u - (mx & 2047u);
+    }
+    // A node whose cover reaches the bound is pruned whatever the remaining rules do
+    // (should_prune tests |S| first and rules only grow S), so the reduction may stop there.
+    __device__ __forceinline__ bool doomed(int pvc, uint32_t k, uint32_t snap) const {
+        return doom || (pvc ? cc > k : cc >= snap);
+    }
+
+    // reduce_loop (reductions.cpp:63-90): rounds of {degree-one, degree-two-triangle,
+    // high-degree} passes, each an ascending scan acting at visit time, until a round changes
+    // nothing. One rolled pass loop; the pass selects the candidate range [lo, hi].
+    template <class Cnt>
+    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st) {
+        while (edges != 0) {
+            ++st.rounds;
+            if (!any_candidate(limit_for(pvc, k, snap, cc))) break;  // the final no-change round
+            bool changed = false;
+#pragma unroll 1
+            for (int pass = 1; pass <= 3; ++pass) {
+                long long t0 = INSTR ? clock64() : 0;
+                uint32_t lo = pass, hi = pass;
+                if (pass == 3) {
+                    const uint32_t lim = limit_for(pvc, k, snap, cc);
+                    // Every alive vertex above the limit at pass start is removed by this pass
+                    // (each removal lowers the limit by one and any degree by at most one), so
+                    // more than `lim` of them take |S| past the bound: the node is pruned.
+                    if (count_above(lim) > lim) doom = true;
+                    lo = lim + 1u;
+                    hi = 0xFFFFu;
+                }
+                int pos = 0;
+#pragma unroll 1
+                while (!doomed(pvc, k, snap)) {
+                    const int v = find_first(pos, lo, hi);
+                    if (v < 0) break;
+                    pos = v + 1;
+                    int u0 = v, u1 = -1;
+                    if (pass < 3) {
+                        int p0, p1;
+                        first_neighbors(v, p0, p1);
+                        u0 = p0;  // degree one: its unique alive neighbour (reductions.cpp:7-19)
+                        if (pass == 2) {  // degree two: both partners iff adjacent (:22-40)
+                            const bool tri = (row_word(p0, p1 >> 5) >> (p1 & 31)) & 1u;
+                            u0 = tri ? p0 : -1;
+                            u1 = tri ? p1 : -1;
+                        }
+                    }
+#pragma unroll 1
+                    for (int t = 0; t < 2; ++t) {
+                        const int u = t ? u1 : u0;
+                        if (u < 0) break;
+                        remove_vertex((uint32_t)u);
+                        changed = true;
+                        st.rm1 += pass == 1;
+                        st.rm2 += pass == 2;
+                        st.rmh += pass == 3;
+                    }
+                    if (pass == 3) lo = limit_for(pvc, k, snap, cc) + 1u;  // :50-56
+                }
+                if (INSTR) st.phase[PH_DEG1 + pass - 1] += clock64() - t0;
+                if (doomed(pvc, k, snap)) return;
+            }
+            if (!changed) break;
+        }
+    }
+
+    // The remove-N(v) child (search_node.cpp:27-32 on a clone) written straight to a record:
+    // d'(w) = d(w) - popc(A[w] & X) for the survivors w, X = N(v) ∩ alive, staged in shared
+    // memory so the word loop stays rolled.
+    // Lane j < W: word j of X = N(v) ∩ alive (the vertices the remove-N(v) child covers).
+    __device__ __forceinline__ uint32_t branch_mask(uint32_t v) const {
+        return lane < W ? (row_word(v, lane) & aw) : 0u;
+    }
+    __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
+                                                unsigned char* rec) const {
+        // X in registers on every lane; xm = this lane's vertices that X removes
+        uint32_t X[W];
+        uint32_t xm = 0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            X[j] = __shfl_sync(FULL, xl, j);
+            xm |= ((X[j] >> lane) & 1u) << j;
+        }
+        const uint32_t keepm = alv & ~xm;  // survivors
+        // rolled pass over vertex words: the survivors' lost degree, parked in shared scratch
+#pragma unroll 1
+        for (int i = 0; i < W; ++i) {
+            uint32_t s = 0;
+            if (__any_sync(FULL, (keepm >> i) & 1u)) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    if ((X[4 * q] | X[4 * q + 1] | X[4 * q + 2] | X[4 * q + 3]) == 0u) continue;
+                    const uint4 c = sat[q * npad + 32 * i + lane];
+                    s += __popc(c.x & X[4 * q]) + __popc(c.y & X[4 * q + 1]) +
+                         __popc(c.z & X[4 * q + 2]) + __popc(c.w & X[4 * q + 3]);
+                }
+            }
+            ss[i * 32 + lane] = s;
+        }
+        uint32_t packed[W / 2];
+        uint32_t esum = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const bool keep = (keepm >> i) & 1u;
+            const uint32_t nd = keep ? d[i] - ss[i * 32 + lane] : 0xFFFFu;  // own writes: no sync
+            esum += keep ? nd : 0u;
+            if (i & 1) packed[i / 2] |= nd << 16;
+            else packed[i / 2] = nd;
+        }
+        const uint32_t e2 = __reduce_add_sync(FULL, esum);
+        if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc + xcnt, e2 / 2);
+        store_degrees(rec, packed);
+        __syncwarp();
+    }
+    __device__ __forceinline__ void store_degrees(unsigned char* rec, const uint32_t* packed) const {
+        unsigned char* p = rec + 16 + lane * (2 * W);
+        if constexpr (W == 4) {
+            *reinterpret_cast<uint2*>(p) = make_uint2(packed[0], packed[1]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < W / 8; ++t)
+                reinterpret_cast<uint4*>(p)[t] =
+                    make_uint4(packed[4 * t], packed[4 * t + 1], packed[4 * t + 2], packed[4 * t + 3]);
+        }
+    }
+    __device__ __forceinline__ void store_current(unsigned char* rec) const {
+        uint32_t packed[W / 2];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t h = alive(i) ? d[i] : 0xFFFFu;
+            if (i & 1) packed[i / 2] |= h << 16;
+            else packed[i / 2] = h;
+        }
+        if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc, edges);
+        store_degrees(rec, packed);
+    }
+    // Moves one record between stack and worklist memory without unpacking it.
+    __device__ __forceinline__ void copy_record(const unsigned char* src, unsigned char* dst) const {
+        const unsigned char* p = src + 16 + lane * (2 * W);
+        unsigned char* q = dst + 16 + lane * (2 * W);
+        if constexpr (W == 4) {
+            *reinterpret_cast<uint2*>(q) = __ldcg(reinterpret_cast<const uint2*>(p));
+        } else {
+#pragma unroll
+            for (int t = 0; t < W / 8; ++t)
+                reinterpret_cast<uint4*>(q)[t] = __ldcg(reinterpret_cast<const uint4*>(p) + t);
+        }
+        if (lane == 0) *reinterpret_cast<uint4*>(dst) = __ldcg(reinterpret_cast<const uint4*>(src));
+    }
+    // Loads a record through L2 (it may come from another SM's worklist donation).
+    __device__ __forceinline__ void load(const unsigned char* rec) {
+        uint32_t packed[W / 2];
+        const unsigned char* p = rec + 16 + lane * (2 * W);
+        if constexpr (W == 4) {
+            const uint2 t = __ldcg(reinterpret_cast<const uint2*>(p));
+            packed[0] = t.x;
+            packed[1] = t.y;
+        } else {
+#pragma unroll
+            for (int t = 0; t < W / 8; ++t) {
+                const uint4 r = __ldcg(reinterpret_cast<const uint4*>(p) + t);
+                packed[4 * t] = r.x;
+                packed[4 * t + 1] = r.y;
+                packed[4 * t + 2] = r.z;
+                packed[4 * t + 3] = r.w;
+            }
+        }
+        uint2 h = make_uint2(0, 0);
+        if (lane == 0) h = __ldcg(reinterpret_cast<const uint2*>(rec));
+        cc = __shfl_sync(FULL, h.x, 0);
+        edges = __shfl_sync(FULL, h.y, 0);
+        doom = false;
+        alv = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t x = (i & 1) ? (packed[i / 2] >> 16) : (packed[i / 2] & 0xFFFFu);
+            d[i] = x;
+            alv |= (x != 0xFFFFu ? 1u : 0u) << i;
+        }
+        rebuild_aw();
+    }
+    // Word `lane` (< W) of the cover bitmap; bits of padding vertices (id >= n) are set and
+    // are masked by the host.
+    __device__ __forceinline__ uint32_t cover_word() const {
+        uint32_t mine = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t b = __ballot_sync(FULL, !alive(i));
+            if (lane == i) mine = b;
+        }
+        return mine;
+    }
+};
+
+// ------------------------------------------------------------------ device worklist
+
+// GlobalWorklist::try_add (worklist.cpp:11-19): reserve capacity in the packed word (also
+// counting the item in `pending` before anyone can see it), then draw a ticket. Two always-
+// succeeding atomics; CAS loops collapse under thousands of contending warps.
+__device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long& pos_out,
+                                          unsigned long long& size_seen) {
+    Ctl* ctl = a.ctl;
+    const unsigned long long old = atomicAdd(&ctl->work, ONE_PENDING | 1ull);
+    const uint32_t size = (uint32_t)old;
+    if (size >= a.capacity) {
+        atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);  // undo: try_add rejects
+        return false;
+    }
+    size_seen = size + 1ull;
+    pos_out = atomicAdd(&ctl->tail, 1ull);
+    return true;
+}
+
+// ------------------------------------------------------------------ the traversal kernel
+
+template <int W, bool INSTR>
+__global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_kernel(DenseArgs a) {
+    extern __shared__ uint4 smem[];
+    constexpr int Q = W / 4;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const uint32_t worker = blockIdx.x * (blockDim.x >> 5) + wib;
+
+    // Stage the read-only adjacency bitmap once per CTA (coalesced 16-byte copies).
+    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) smem[t] = a.at4[t];
+    __syncthreads();
+    if (worker >= a.workers) return;
+
+    const unsigned long long t_start = globaltimer();
+    const long long c_start = clock64();
+    WarpNode<W, INSTR> x;
+    x.sat = smem;
+    x.sx = smem + Q * a.npad + wib * Q;
+    x.ss = reinterpret_cast<uint32_t*>(smem + Q * a.npad + (blockDim.x >> 5) * Q) + wib * W * 32;
+    x.npad = a.npad;
+    x.lane = lane;
+    Counters st;
+    Ctl* ctl = a.ctl;
+    unsigned char* const my_stack =
+        a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes;
+    // The local stack is a ring [base, base + sp) so its oldest entry can be donated.
+    uint32_t base = 0, sp = 0;
+    auto slot_at = [&](uint32_t i) {
+        uint32_t j = base + i;
+        if (j >= a.stack_bound) j -= a.stack_bound;
+        return my_stack + (unsigned long long)j * a.entry_bytes;
+    };
+    bool have = false, idle = true;
+    uint32_t best = a.pvc ? a.k : ctl->best;
+    unsigned long long nodes_flushed = 0;
+
+#pragma unroll 1
+    while (true) {
+        if (!have) {
+            long long t0 = INSTR ? clock64() : 0;
+            const unsigned char* src;
+            unsigned long long* release = nullptr;
+            unsigned long long pos = 0;
+            if (sp > 0) {
+                --sp;
+                src = slot_at(sp);
+            } else {
+                // GlobalWorklist::remove_or_done (worklist.cpp:21-48): take a ticket, then wait
+                // for that slot's publication, for termination (pending == 0) or a cancel.
+                if (!idle) {
+                    if (lane == 0) atomicAdd(&ctl->work, ~ONE_PENDING + 1ull);  // pending - 1
+                    idle = true;
+                }
+                if (lane == 0) pos = atomicAdd(&ctl->head, 1ull);
+                pos = __shfl_sync(FULL, pos, 0);
+                release = a.seq + (pos & a.ring_mask);
+                uint32_t sleep = 32;
+                int outcome = 0;  // 1 got, 2 done
+#pragma unroll 1
+                for (uint32_t spin = 0;; ++spin) {
+                    int o = 0;
+                    if (lane == 0) {
+                        if (ld_acquire_u64(release) == pos + 1) o = 1;
+                        else if ((spin & 7) == 7) {
+                            if (ld_volatile_v4(ctl).y) o = 2;
+                            else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0) o = 2;
+                            else if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+                        }
+                    }
+                    outcome = __shfl_sync(FULL, o, 0);
+                    if (outcome) break;
+                    __nanosleep(sleep);
+                    sleep = min(sleep * 2, a.backoff_ns);
+                }
+                if (outcome == 2) {
+                    if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
+                    break;
+                }
+                (void)ld_acquire_u64(release);  // every lane acquires the publication
+                src = a.wl + (pos & a.ring_mask) * a.entry_bytes;
+                idle = false;
+            }
+            x.load(src);
+            if (release) {
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    st_release_u64(release, pos + a.ring_mask + 1);  // free for the next lap
+                    atomicAdd(&ctl->work, ~0ull);                     // size - 1
+                }
+            }
+            have = true;
+            if (INSTR) st.phase[release ? PH_WL_REMOVE : PH_STACK] += clock64() - t0;
+        }
+
+        // Issue the read of the hot control line now, consume it after the reduction (its L2
+        // latency hides behind the rule passes). The rules use the bound seen at the previous
+        // node (a stale, larger bound only prunes less).
+        uint4 h = make_uint4(0, 0, 0, 0);
+        unsigned long long hw = 0;
+        if (lane == 0) {
+            h = ld_volatile_v4(ctl);
+            hw = ld_relaxed_u64(&ctl->work);
+        }
+
+        // visit_and_check_limits (scheduler.cpp:63-74), batched per flush_every visits
+        ++st.nodes;
+        if (st.nodes - nodes_flushed >= a.flush_every) {
+            int stop = 0;
+            if (lane == 0) {
+                const unsigned long long tot =
+                    atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed) + (st.nodes - nodes_flushed);
+                if (a.node_budget && tot > a.node_budget) stop = 2;
+                else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) stop = 1;
+                if (stop) {
+                    atomicCAS(&ctl->status, 0, stop);
+                    atomicExch(&ctl->cancel, 1u);
+                }
+                if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+            }
+            nodes_flushed = st.nodes;
+            if (__shfl_sync(FULL, stop, 0)) break;
+        }
+
+        // process_node (scheduler.cpp:125-144)
+        x.reduce(a.pvc, a.k, best, st);
+        if (__shfl_sync(FULL, h.y, 0)) break;
+        if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
+        const uint32_t qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+        const bool prune = x.doom || should_prune(a.pvc, a.k, best, x.cc, x.edges);
+        st.dooms += x.doom;
+        if (prune) {
+            have = false;
+            continue;
+        }
+        if (x.edges == 0) {
+            // record_cover (scheduler.cpp:84-108)
+            uint32_t record = 0;
+            if (lane == 0) {
+                if (a.pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
+                else record = x.cc < atomicMin(&ctl->best, x.cc);
+            }
+            if (__shfl_sync(FULL, record, 0)) {
+                const uint32_t wbits = x.cover_word();
+                if (lane < W) a.cover_slots[(unsigned long long)worker * W + lane] = wbits;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    atomicMin(&ctl->best_owner, ((unsigned long long)x.cc << 32) | worker);
+                    if (a.pvc) atomicExch(&ctl->cancel, 1u);
+                    if (a.mailbox) {
+                        a.mailbox[2] = x.cc;
+                        if (a.pvc) a.mailbox[3] = 1;
+                    }
+                }
+            }
+            if (a.pvc) break;  // the search is ended (solver_seq.cpp:108)
+            best = min(best, x.cc);
+            have = false;
+            continue;
+        }
+        long long tm = INSTR ? clock64() : 0;
+        const uint32_t v = x.argmax();
+        ++st.maxdeg;
+        if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
+
+        // Branch (scheduler.cpp:185-203): defer remove-N(v) — donated while the worklist is
+        // below its threshold (with donate_oldest the oldest stacked node goes instead and the
+        // child is stacked) — and continue with remove-v.
+        long long tb = INSTR ? clock64() : 0;
+        unsigned char* child = nullptr;
+        unsigned long long* publish = nullptr;
+        unsigned long long pos = 0;
+        // (After a full reduction every alive degree is within the high-degree limit, so
+        // |S| + |N(v)| stays below the bound: the deferred child is never dead on arrival.)
+        const uint32_t xl = x.branch_mask(v);
+        const uint32_t xcnt = __reduce_add_sync(FULL, __popc(xl));
+        const bool oldest = a.donate_oldest && sp > 0;
+        if (!a.seq_mode && qsize < a.threshold) {
+            unsigned long long seen = 0;
+            int ok = 0;
+            if (lane == 0) ok = q_reserve(a, pos, seen);
+            if (__shfl_sync(FULL, ok, 0)) {
+                pos = __shfl_sync(FULL, pos, 0);
+                publish = a.seq + (pos & a.ring_mask);
+                if (lane == 0) {
+                    st.max_queue = max(st.max_queue, seen);
+                    // the slot is free once the previous lap's reader released it
+                    while (ld_acquire_u64(publish) != pos) __nanosleep(32);
+                }
+                __syncwarp();
+                unsigned char* dst = a.wl + (pos & a.ring_mask) * a.entry_bytes;
+                if (oldest) {
+                    x.copy_record(slot_at(0), dst);
+                    base = base + 1 == a.stack_bound ? 0 : base + 1;
+                    --sp;
+                } else {
+                    child = dst;
+                }
+                ++st.donated;
+            }
+        }
+        if (!child) {
+            child = slot_at(sp);
+            ++sp;
+            if (sp > st.high_water) st.high_water = sp;
+        }
+        x.write_child(xl, xcnt, child);
+        ++st.children;
+        if (publish) {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release_u64(publish, pos + 1);
+        }
+        if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
+        long long tv = INSTR ? clock64() : 0;
+        x.remove_vertex(v);
+        if (INSTR) st.phase[PH_BRANCH_V] += clock64() - tv;
+    }
+
+    if (lane == 0) {
+        if (st.nodes > nodes_flushed) atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed);
+        WStats o;
+        o.nodes = st.nodes;
+        o.rounds = st.rounds;
+        o.maxdeg = st.maxdeg;
+        o.children = st.children;
+        o.rm1 = st.rm1;
+        o.rm2 = st.rm2;
+        o.rmh = st.rmh;
+        o.dooms = st.dooms;
+        o.high_water = st.high_water;
+        o.donated = st.donated;
+        o.active = clock64() - c_start;
+        o.max_queue = st.max_queue;
+#pragma unroll
+        for (int p = 0; p < 10; ++p) o.phase[p] = INSTR ? st.phase[p] : 0ull;
+        a.stats[worker] = o;
+    }
+}
+
+// ------------------------------------------------------------------ frontier expansion
+
+// Level-synchronous expansion (multi-GPU partitioning): warp i processes node i
+// of a level exactly as process_node does (scheduler.cpp:125-144) with a FIXED bound, and writes
+// its remove-N(v) child to out[2i] and its remove-v child to out[2i+1]. The result does not
+// depend on scheduling, so every rank derives the same frontier.
+struct ExpandArgs {
+    const uint4* at4;
+    uint32_t n, npad;
+    int pvc;
+    uint32_t k, best;
+    uint32_t count;
+    unsigned long long entry_bytes;
+    const unsigned char* in;
+    unsigned char* out;
+    uint32_t* flags;   // per input: 0 pruned, 1 cover found, 2 branched
+    uint32_t* covers;  // per input: [cc, bitmap W words]
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
+    extern __shared__ uint4 smem[];
+    constexpr int Q = W / 4;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) smem[t] = a.at4[t];
+    __syncthreads();
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    WarpNode<W, false> x;
+    x.sat = smem;
+    x.sx = smem + Q * a.npad + (threadIdx.x >> 5) * Q;
+    x.ss = reinterpret_cast<uint32_t*>(smem + Q * a.npad + (blockDim.x >> 5) * Q) +
+           (threadIdx.x >> 5) * W * 32;
+    x.npad = a.npad;
+    x.lane = lane;
+    Counters st;
+#pragma unroll 1
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < a.count; i += warps) {
+        x.load(a.in + (unsigned long long)i * a.entry_bytes);
+        x.reduce(a.pvc, a.k, a.best, st);
+        uint32_t flag;
+        if (x.doom || should_prune(a.pvc, a.k, a.best, x.cc, x.edges)) {
+            flag = 0;
+        } else if (x.edges == 0) {
+            flag = 1;
+            uint32_t* c = a.covers + (unsigned long long)i * (W + 1);
+            const uint32_t wbits = x.cover_word();
+            if (lane < W) c[1 + lane] = wbits;
+            if (lane == 0) c[0] = x.cc;
+        } else {
+            flag = 2;
+            const uint32_t v = x.argmax();
+            const uint32_t xl = x.branch_mask(v);
+            x.write_child(xl, __reduce_add_sync(FULL, __popc(xl)), a.out + (2ull * i) * a.entry_bytes);
+            x.remove_vertex(v);
+            x.store_current(a.out + (2ull * i + 1) * a.entry_bytes);
+        }
+        if (lane == 0) a.flags[i] = flag;
+    }
+}
+
+}  // namespace vcg

@@ -181,6 +181,8 @@ def test_frontier_shards_cover_the_tree_exactly(config_golden, name, k_key, worl
     total = fr["nodes"]
     for rank in range(world):
         share = fr["seeds"][rank::world]
+        if len(share) == 0:  # nothing to search on this rank (solve_distributed skips it too)
+            continue
         r = vc.solve_pvc(g, k, strategy="gpu", seeds=share)
         assert not r["feasible"]
         total += r["nodes_total"]
