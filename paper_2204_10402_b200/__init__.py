@@ -190,18 +190,21 @@ def load_graph(path, fmt=None, complement_input=False) -> BaseGraph:
 _STRATEGIES = {"hybrid": _n.VCG_HYBRID, "gpu": _n.VCG_HYBRID, "seq": _n.VCG_SEQ,
                "stackonly": _n.VCG_STACKONLY}
 _RULES = {"reference": 0, "parallel": 1}
+_ENGINES = {"auto": 0, "dense": 1, "sparse": 2}
 
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
-           timeout_s, node_budget, device, rules, block_warps, instrument, initial_best=0,
-           seeds=None, mailbox=None, raw=False, donate_oldest=None, stream=None):
+           timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
+           instrument=False, initial_best=0, seeds=None, mailbox=None, raw=False,
+           donate_oldest=None, stream=None, engine="auto"):
+    """The strategy dispatch of bindings.cpp:60-99, on the GPU through vcg_solve."""
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
+    if engine not in _ENGINES:
+        raise ValueError(f"unknown engine: {engine}")
     if workers is None:
         workers = {"hybrid": 4, "gpu": 0, "seq": 1, "stackonly": 4}[strategy]
-    if workers < 0:
-        raise ValueError("num_workers must be >= 1")
-    if strategy != "gpu" and workers < 1:
+    if workers < 0 or (strategy != "gpu" and workers < 1):
         raise ValueError("num_workers must be >= 1")  # scheduler.cpp:21
     p = _n.Params()
     _lib.vcg_params_init(C.byref(p))
@@ -218,6 +221,7 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
     p.device = device
     p.rules = _RULES[rules]
     p.block_warps = block_warps
+    p.engine = _ENGINES[engine]
     p.instrument = int(bool(instrument))
     if donate_oldest is None:  # the tuned GPU policy for "gpu"; the reference policy for "hybrid"
         donate_oldest = strategy == "gpu"
@@ -270,22 +274,21 @@ def _result_dict(r):
 
 
 def solve_mvc(graph, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
-              depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
-              rules="reference", block_warps=0, instrument=False, initial_best=0, seeds=None,
-              mailbox=None, raw=False, donate_oldest=None, stream=None):
-    """Solve MVC; returns the run report as a dict (bindings.cpp:174-187)."""
+              depth=8, backoff_us=50, timeout_s=None, node_budget=None, **gpu):
+    """Solve MVC; returns the run report as a dict (bindings.cpp:174-187).
+
+    GPU keyword knobs: device, engine ("auto" | "dense" | "sparse"), rules, block_warps,
+    instrument, donate_oldest, initial_best, seeds, mailbox, stream, raw."""
     return _solve(graph, "mvc", 0, strategy, workers, capacity, threshold_fraction, depth,
-                  backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  initial_best, seeds, mailbox, raw, donate_oldest, stream)
+                  backoff_us, timeout_s, node_budget, **gpu)
 
 
 def solve_pvc(graph, k, strategy="hybrid", workers=None, capacity=4096, threshold_fraction=0.5,
-              depth=8, backoff_us=50, timeout_s=None, node_budget=None, *, device=0,
-              rules="reference", block_warps=0, instrument=False, seeds=None, mailbox=None,
-              raw=False, donate_oldest=None, stream=None):
+              depth=8, backoff_us=50, timeout_s=None, node_budget=None, **gpu):
     """Solve PVC for a given k; returns the run report as a dict (bindings.cpp:188-202)."""
     if k < 1:
         raise ValueError("pvc requires k >= 1")  # bindings.cpp:194
+    if "initial_best" in gpu:
+        raise TypeError("initial_best applies to MVC only")
     return _solve(graph, "pvc", k, strategy, workers, capacity, threshold_fraction, depth,
-                  backoff_us, timeout_s, node_budget, device, rules, block_warps, instrument,
-                  0, seeds, mailbox, raw, donate_oldest, stream)
+                  backoff_us, timeout_s, node_budget, **gpu)

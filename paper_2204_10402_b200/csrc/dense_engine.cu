@@ -41,6 +41,7 @@
 #include <vector>
 
 #include "dense_kernels.cuh"
+#include "sparse_kernels.cuh"
 #include "engine.hpp"
 
 namespace vcg {
@@ -58,10 +59,15 @@ namespace vcg {
 struct DeviceGraph {
     int device = -1;
     uint32_t W = 0, npad = 0;
-    uint4* at4 = nullptr;
+    uint4* at4 = nullptr;       // dense engine: adjacency bitmap
     size_t at4_bytes = 0;
+    uint32_t* off = nullptr;    // sparse engine: CSR with u32 offsets
+    uint32_t* nbr = nullptr;
+    size_t csr_bytes = 0;
     ~DeviceGraph() {
         if (at4) cudaFree(at4);
+        if (off) cudaFree(off);
+        if (nbr) cudaFree(nbr);
     }
 };
 
@@ -82,7 +88,7 @@ struct Arena {
     }
 };
 struct DeviceCtx {
-    Arena stacks, wl, seq, misc;
+    Arena stacks, wl, seq, misc, scratch;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
@@ -185,7 +191,10 @@ int device_count() {
     return n;
 }
 
+static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out);
+
 void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
+    if (s.engine == 2 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
     if (g.n > 1024)
         throw std::invalid_argument("graph has " + std::to_string(g.n) +
                                     " vertices; the dense engine handles n <= 1024");
@@ -374,6 +383,208 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
             if ((bits[v >> 5] >> (v & 31)) & 1u) out.cover.push_back(v);
     }
 }
+
+// ------------------------------------------------------------------ sparse engine host side
+
+static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
+    const int dev = s.device;
+    const int ndev = device_count();
+    if (ndev == 0) throw std::runtime_error("CUDA error: no CUDA device visible");
+    if (dev < 0 || dev >= ndev) throw std::invalid_argument("device ordinal out of range");
+    if (2 * g.m >= (1ull << 32)) throw std::invalid_argument("graph too large for u32 CSR offsets");
+    CUDA_CHECK(cudaSetDevice(dev));
+    DeviceCtx& C = ctx_for(dev);
+    cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
+
+    uint32_t maxdeg = 0;
+    for (uint32_t v = 0; v < g.n; ++v) maxdeg = std::max(maxdeg, g.degree(v));
+    if (maxdeg >= 0xFFFFu) throw std::invalid_argument("sparse engine: degree >= 65535");
+    const uint32_t npad = (g.n + 7) / 8 * 8;
+    const size_t entry = 16 + 2 * (size_t)npad;
+    const size_t smem = 2 * (size_t)npad + (2 * SP_THREADS + 1) * 4;
+    int max_smem = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (smem + sizeof(SpShared) + 1024 > (size_t)max_smem)
+        throw std::invalid_argument("graph has " + std::to_string(g.n) +
+                                    " vertices; the shared-memory degree array holds at most " +
+                                    std::to_string((max_smem - 12 * 1024) / 2));
+    out.engine = 2;
+    out.degree_bytes = 2;
+    out.n_padded = npad;
+
+    auto th0 = std::chrono::steady_clock::now();
+    if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
+    if (!g.dev[dev] || !g.dev[dev]->off) {
+        auto dg = g.dev[dev] ? g.dev[dev] : std::make_shared<DeviceGraph>();
+        dg->device = dev;
+        std::vector<uint32_t> off32(g.n + 1);
+        for (uint32_t v = 0; v <= g.n; ++v) off32[v] = (uint32_t)g.off[v];
+        CUDA_CHECK(cudaMalloc(&dg->off, off32.size() * 4));
+        CUDA_CHECK(cudaMalloc(&dg->nbr, std::max<size_t>(1, g.nbr.size()) * 4));
+        CUDA_CHECK(cudaMemcpyAsync(dg->off, off32.data(), off32.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!g.nbr.empty())
+            CUDA_CHECK(cudaMemcpyAsync(dg->nbr, g.nbr.data(), g.nbr.size() * 4, cudaMemcpyHostToDevice, st));
+        dg->csr_bytes = off32.size() * 4 + g.nbr.size() * 4;
+        out.h2d_bytes += dg->csr_bytes;
+        g.dev[dev] = dg;
+    }
+    const DeviceGraph& dg = *g.dev[dev];
+
+    uint32_t workers = s.workers;
+    if (s.strategy == 1) workers = 1;
+    if (workers == 0) workers = (uint32_t)C.sms;  // one CTA (a 1024-thread worker) per SM
+    out.grid = workers;
+    out.block = SP_THREADS;
+
+    // stack depth: the reference bound (greedy / min(k, n)), capped by device memory
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(s.capacity, s.num_seeds), 1);
+    uint64_t ring = 2;
+    while (ring < cap) ring <<= 1;
+    const size_t scratch_bytes = (size_t)workers * g.n * (8 * 4 + 8 + 4);
+    const size_t fixed = ring * entry + ring * 8 + scratch_bytes + (64ull << 20);
+    if (fixed >= free_b) throw std::runtime_error("CUDA error: out of device memory for the worklist");
+    const uint64_t by_mem = (uint64_t)((free_b - fixed) * 0.6 / ((double)workers * entry));
+    uint32_t bound = (uint32_t)std::min<uint64_t>((uint64_t)std::max<uint32_t>(s.stack_bound, 1) + 1,
+                                                  std::max<uint64_t>(by_mem, 2));
+    unsigned char* stacks = (unsigned char*)C.stacks.get((size_t)workers * bound * entry);
+    unsigned char* wl = (unsigned char*)C.wl.get(ring * entry);
+    unsigned long long* seq = (unsigned long long*)C.seq.get(ring * 8);
+    const uint32_t cover_words = (g.n + 31) / 32;
+    const size_t slots_bytes = ((size_t)workers * cover_words * 4 + 255) / 256 * 256;
+    unsigned char* misc = (unsigned char*)C.misc.get(sizeof(Ctl) + slots_bytes + (size_t)workers * sizeof(WStats));
+    Ctl* ctl = reinterpret_cast<Ctl*>(misc);
+    uint32_t* cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
+    WStats* stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
+    unsigned char* scr = (unsigned char*)C.scratch.get(scratch_bytes);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(scr);
+    unsigned long long* owner = reinterpret_cast<unsigned long long*>(scr + (size_t)workers * g.n * 32);
+    uint32_t* tag = reinterpret_cast<uint32_t*>(scr + (size_t)workers * g.n * 40);
+    CUDA_CHECK(cudaMemsetAsync(scr, 0, (size_t)workers * g.n * 32, st));              // lists, cnt = 0
+    CUDA_CHECK(cudaMemsetAsync(owner, 0xFF, (size_t)workers * g.n * 8, st));           // no claims
+    CUDA_CHECK(cudaMemsetAsync(tag, 0, (size_t)workers * g.n * 4, st));
+
+    // initial worklist: root (init_root) or the seeds, as u16 records
+    const uint64_t nseeds = s.num_seeds ? s.num_seeds : 1;
+    std::vector<unsigned char> recs(nseeds * entry, 0);
+    for (uint64_t i = 0; i < nseeds; ++i) {
+        unsigned char* rec = recs.data() + i * entry;
+        uint32_t* h = reinterpret_cast<uint32_t*>(rec);
+        uint16_t* dd = reinterpret_cast<uint16_t*>(rec + 16);
+        if (s.num_seeds) {
+            const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
+            h[0] = r[0];
+            h[1] = r[1];
+            for (uint32_t v = 0; v < g.n; ++v) dd[v] = r[2 + v] == REM ? DREM : (uint16_t)r[2 + v];
+        } else {
+            h[0] = 0;
+            h[1] = (uint32_t)g.m;
+            for (uint32_t v = 0; v < g.n; ++v) dd[v] = (uint16_t)g.degree(v);
+        }
+        for (uint32_t v = g.n; v < npad; ++v) dd[v] = DREM;
+    }
+    Ctl hc;
+    std::memset(&hc, 0, sizeof(hc));
+    hc.best = s.best;
+    hc.tail = nseeds;
+    hc.work = (nseeds << 32) | nseeds;
+    hc.best_owner = ~0ull;
+    CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+    init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
+    out.h2d_bytes += sizeof(hc) + recs.size();
+    out.launches += 2;
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    out.h2d_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+
+    SparseArgs a;
+    a.off = dg.off;
+    a.nbr = dg.nbr;
+    a.n = g.n;
+    a.npad = npad;
+    a.pvc = s.pvc ? 1 : 0;
+    a.k = s.k;
+    a.capacity = (uint32_t)cap;
+    a.ring_mask = (uint32_t)(ring - 1);
+    a.threshold = (uint32_t)std::min<uint64_t>(s.threshold, cap);
+    a.workers = workers;
+    a.stack_bound = bound;
+    a.entry_bytes = entry;
+    a.stacks = stacks;
+    a.wl = wl;
+    a.seq = seq;
+    a.ctl = ctl;
+    a.cover_slots = cover_slots;
+    a.cover_words = cover_words;
+    a.stats = stats;
+    a.scratch = scratch;
+    a.owner = owner;
+    a.tag = tag;
+    a.node_budget = s.node_budget;
+    a.timeout_ns = s.timeout_s >= 0 ? (unsigned long long)(s.timeout_s * 1e9) : 0ull;
+    if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
+    a.flush_every = s.node_budget ? 1 : 16;
+    a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
+    a.seq_mode = s.strategy == 1 ? 1 : 0;
+    a.donate_oldest = s.donate_oldest ? 1 : 0;
+    a.mailbox = s.mailbox;
+
+    CUDA_CHECK(cudaFuncSetAttribute(sparse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaEventRecord(C.ev0, st));
+    sparse_kernel<false><<<workers, SP_THREADS, smem, st>>>(a);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaEventRecord(C.ev1, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
+    out.device_ms = ms;
+
+    CUDA_CHECK(cudaMemcpy(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+    if (hc.status == 3)
+        throw std::runtime_error("CUDA error: search stack depth exceeded the device-memory cap (" +
+                                 std::to_string(bound) + " nodes per worker)");
+    std::vector<WStats> hs(workers);
+    CUDA_CHECK(cudaMemcpy(hs.data(), stats, workers * sizeof(WStats), cudaMemcpyDeviceToHost));
+    out.d2h_bytes += sizeof(hc) + workers * sizeof(WStats);
+    out.status = hc.status;
+    out.wl_added = hc.tail;
+    out.wl_current = (uint32_t)hc.work;
+    out.wl_removed = hc.tail - out.wl_current;
+    out.wl_max_size = nseeds;
+    out.worker_nodes.resize(workers);
+    out.worker_high_water.resize(workers);
+    for (uint32_t w = 0; w < workers; ++w) {
+        out.worker_nodes[w] = hs[w].nodes;
+        out.worker_high_water[w] = hs[w].high_water;
+        out.rounds += hs[w].rounds;
+        out.maxdeg += hs[w].maxdeg;
+        out.children += hs[w].children;
+        out.removals += hs[w].rm1 + hs[w].rm2 + hs[w].rmh;
+        out.rm1 += hs[w].rm1;
+        out.rm2 += hs[w].rm2;
+        out.rmh += hs[w].rmh;
+        out.dooms += hs[w].dooms;
+        out.donated += hs[w].donated;
+        out.active_cycles += hs[w].active;
+        out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
+    }
+    if (hc.best_owner != ~0ull) {
+        const uint32_t ow = (uint32_t)(hc.best_owner & 0xFFFFFFFFu);
+        out.found = true;
+        out.found_size = (uint32_t)(hc.best_owner >> 32);
+        std::vector<uint32_t> bits(cover_words);
+        CUDA_CHECK(cudaMemcpy(bits.data(), cover_slots + (size_t)ow * cover_words, cover_words * 4,
+                              cudaMemcpyDeviceToHost));
+        out.d2h_bytes += cover_words * 4;
+        out.cover.clear();
+        for (uint32_t v = 0; v < g.n; ++v)
+            if ((bits[v >> 5] >> (v & 31)) & 1u) out.cover.push_back(v);
+    }
+}
+
 
 void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f) {
     if (g.n > 1024)

@@ -7,6 +7,7 @@ rules in the reference's order: the 1-worker ("seq") traversal visits exactly th
 solve_seq node count, and PVC no-instance trees are schedule independent, so every worker
 count reproduces the reference node count.
 """
+import numpy as np
 import pytest
 
 import paper_2204_10402_b200 as vc
@@ -210,3 +211,79 @@ def test_mailbox_cancel_and_external_bound():
     r = vc.solve_pvc(g, 482, strategy="gpu", mailbox=mb.address)
     assert r["nodes_total"] < 21461369
     mb.close()
+
+
+# ---- sparse engine (one CTA per node, block-parallel rule rounds) -------------------------
+
+@pytest.mark.parametrize("workers", [1, 3, None])
+def test_sparse_engine_corpus_exact(corpus, workers):
+    """The block-parallel rules are sound: MVC sizes equal the brute-force optimum on all 535
+    corpus graphs (forced onto the sparse engine)."""
+    bad = []
+    for it in corpus:
+        g = graph_of(it)
+        r = vc.solve_mvc(g, strategy="gpu" if workers is None else "hybrid", workers=workers,
+                         engine="sparse")
+        check_cover(g, r)
+        if r["size"] != it["mvc"] or r["status"] != "complete" or r["engine"] != 2:
+            bad.append((it["name"], r["size"], it["mvc"]))
+    assert not bad, bad[:10]
+
+
+def test_sparse_engine_pvc_triple(corpus):
+    bad = []
+    for it in corpus[::2]:
+        g = graph_of(it)
+        for p in it["pvc"]:
+            r = vc.solve_pvc(g, p["k"], strategy="gpu", engine="sparse")
+            ok = r["feasible"] == p["feasible"]
+            if r["feasible"]:
+                check_cover(g, r)
+                ok = ok and r["size"] <= p["k"]
+            if not ok:
+                bad.append((it["name"], p, r["feasible"]))
+    assert not bad, bad[:10]
+
+
+def _random_tree(n, seed):
+    rng = np.random.default_rng(seed)
+    return [(int(rng.integers(0, v)), v) for v in range(1, n)]
+
+
+@pytest.mark.parametrize("n,seed", [(3000, 1), (20000, 2)])
+def test_sparse_engine_large_trees_equal_oracle(oracle, n, seed):
+    """n > 1024 (auto-selects the sparse engine); trees are solved exactly by the rules."""
+    from oracle.oracle import CSR
+    edges = _random_tree(n, seed)
+    g = vc.make_graph(n, edges)
+    r = vc.solve_mvc(g, strategy="gpu")
+    assert r["engine"] == 2
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(n, g.num_edges, off, nbr))
+    assert r["size"] == want["size"]
+    check_cover(g, r)
+
+
+def test_sparse_engine_sparse_random_graph(oracle):
+    from oracle.oracle import CSR
+    rng = np.random.default_rng(5)
+    n = 1500
+    m = int(1.1 * n)
+    e = rng.integers(0, n, size=(m, 2))
+    g = vc.make_graph(n, [tuple(map(int, x)) for x in e])
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(n, g.num_edges, off, nbr), node_budget=2_000_000)
+    assert want["status"] == "complete"
+    r = vc.solve_mvc(g, strategy="gpu")
+    assert r["size"] == want["size"] and r["status"] == "complete"
+    check_cover(g, r)
+    no = vc.solve_pvc(g, want["size"] - 1, strategy="gpu")
+    assert not no["feasible"]
+
+
+def test_c4_budgeted_run(config_golden):
+    g = load_config("c4")
+    r = vc.solve_mvc(g, strategy="gpu", node_budget=3000)
+    assert r["engine"] == 2 and r["status"] == "budget"
+    assert r["size"] <= config_golden["c4"]["greedy"]
+    check_cover(g, r)
