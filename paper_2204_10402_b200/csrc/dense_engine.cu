@@ -442,7 +442,8 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(s.capacity, s.num_seeds), 1);
     uint64_t ring = 2;
     while (ring < cap) ring <<= 1;
-    const size_t scratch_bytes = (size_t)workers * g.n * (8 * 4 + 8 + 4);
+    // per worker: 10n u32 lists, n u32 counters, n u64 claims, n u32 tags
+    const size_t scratch_bytes = (size_t)workers * g.n * (10 * 4 + 4 + 8 + 4);
     const size_t fixed = ring * entry + ring * 8 + scratch_bytes + (64ull << 20);
     if (fixed >= free_b) throw std::runtime_error("CUDA error: out of device memory for the worklist");
     const uint64_t by_mem = (uint64_t)((free_b - fixed) * 0.6 / ((double)workers * entry));
@@ -458,12 +459,14 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     uint32_t* cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
     WStats* stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
     unsigned char* scr = (unsigned char*)C.scratch.get(scratch_bytes);
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(scr);
-    unsigned long long* owner = reinterpret_cast<unsigned long long*>(scr + (size_t)workers * g.n * 32);
-    uint32_t* tag = reinterpret_cast<uint32_t*>(scr + (size_t)workers * g.n * 40);
-    CUDA_CHECK(cudaMemsetAsync(scr, 0, (size_t)workers * g.n * 32, st));              // lists, cnt = 0
-    CUDA_CHECK(cudaMemsetAsync(owner, 0xFF, (size_t)workers * g.n * 8, st));           // no claims
-    CUDA_CHECK(cudaMemsetAsync(tag, 0, (size_t)workers * g.n * 4, st));
+    const size_t wn = (size_t)workers * g.n;
+    unsigned long long* owner = reinterpret_cast<unsigned long long*>(scr);  // 8-aligned first
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(scr + wn * 8);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(scr + wn * 48);
+    uint32_t* tag = reinterpret_cast<uint32_t*>(scr + wn * 52);
+    CUDA_CHECK(cudaMemsetAsync(cnt, 0, wn * 4, st));        // counters start at zero
+    CUDA_CHECK(cudaMemsetAsync(owner, 0xFF, wn * 8, st));   // no triangle claims
+    CUDA_CHECK(cudaMemsetAsync(tag, 0, wn * 4, st));        // epochs start at 1
 
     // initial worklist: root (init_root) or the seeds, as u16 records
     const uint64_t nseeds = s.num_seeds ? s.num_seeds : 1;
@@ -521,6 +524,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     a.cover_words = cover_words;
     a.stats = stats;
     a.scratch = scratch;
+    a.cnt = cnt;
     a.owner = owner;
     a.tag = tag;
     a.node_budget = s.node_budget;

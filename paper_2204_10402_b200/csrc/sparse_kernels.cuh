@@ -11,11 +11,15 @@
 //                    triangles are vertex-disjoint;
 //   * high degree  — every alive vertex above the limit at the snapshot is forced into any
 //                    improving cover containing S, so all are removed at once (and if more than
-//                    the limit exist, the node is pruned — the same exact test as the dense
-//                    engine's).
-// Each phase is sound applied to the snapshot (DESIGN.md §4 has the arguments); the fixpoint
-// conditions are the reference's, so answers (MVC size, PVC yes/no) are exact, while the
-// visited tree — and so node counts — may differ from the reference's sequential order.
+//                    the limit exist, the node is pruned — the dense engine's exact test).
+// Each phase is sound applied to its snapshot; the fixpoint conditions are the
+// reference's, so answers (MVC size, PVC yes/no) are exact, while the visited tree — and so
+// node counts — may differ from the reference's sequential order.
+//
+// Work is incremental: a popped record gets one full scan; after that the candidate lists are
+// fed by the decrement phase itself (a vertex whose degree drops to 1 or 2 is appended), |E|
+// is maintained from the decrements, and the high-degree pass only scans when the max-degree
+// bound exceeds the limit. One closing scan yields the smallest-id max-degree vertex.
 //
 // Layout: u16 degrees (0xFFFF = in the cover) in smem, decremented with 32-bit shared atomics
 // on the containing word; CSR (u32 offsets / neighbours) read through L2; deferred nodes are
@@ -44,9 +48,10 @@ struct SparseArgs {
     uint32_t* cover_slots;    // workers * cover_words
     uint32_t cover_words;     // ceil(n / 32)
     WStats* stats;
-    uint32_t* scratch;        // workers * 8n: L1, L2, L3, RL, T, cnt, P (2n)
+    uint32_t* scratch;        // workers * 8n u32: A1, A2, N1, N2, L3, RL, T, P(2n) ...
     unsigned long long* owner;  // workers * n (triangle claims, epoch-tagged)
-    uint32_t* tag;            // workers * n (branch-set membership, epoch-tagged)
+    uint32_t* tag;            // workers * n (phase / branch-set membership, epoch-tagged)
+    uint32_t* cnt;            // workers * n (per-vertex counters, zero between uses)
     unsigned long long node_budget, timeout_ns, flush_every;
     uint32_t backoff_ns;
     int seq_mode, donate_oldest;
@@ -55,20 +60,17 @@ struct SparseArgs {
 
 // CTA-wide shared control block (decisions are made here and read after a barrier)
 struct SpShared {
-    uint32_t c1, c2, cH, nrem, nT, nX, nA;   // list lengths
+    uint32_t a1, a2, n1, n2, cH, nrem, nT, nX, nA;  // list lengths
     uint32_t scan_total;
-    uint32_t eX, sumX;                        // branch bookkeeping
-    unsigned long long sumdeg, maxkey;        // scan results
-    uint32_t cc, edges, doom;
+    uint32_t eX, ecut;                               // edge bookkeeping
+    unsigned long long sumdeg, maxkey;               // scan results
+    uint32_t cc, edges, doom, maxdeg;
     int outcome;
     unsigned long long pos;
-    uint32_t red[32];                         // block reductions
-    unsigned long long red64[32];
+    uint32_t red[32];
 };
 
 // ---------------------------------------------------------------- block-level helpers
-
-__device__ __forceinline__ uint16_t dget(const uint16_t* deg, uint32_t v) { return deg[v]; }
 
 // atomically set deg[v] = 0xFFFF; returns the previous value
 __device__ __forceinline__ uint32_t dclaim(uint16_t* deg, uint32_t v) {
@@ -77,20 +79,23 @@ __device__ __forceinline__ uint32_t dclaim(uint16_t* deg, uint32_t v) {
     const uint32_t old = atomicOr(w, 0xFFFFu << sh);
     return (old >> sh) & 0xFFFFu;
 }
-// deg[v] -= 1 for an alive v (never borrows: an alive neighbour has degree >= 1)
-__device__ __forceinline__ void ddec(uint16_t* deg, uint32_t v) {
+// deg[v] -= 1 for an alive v (never borrows: an alive neighbour has degree >= 1);
+// returns the new degree
+__device__ __forceinline__ uint32_t ddec(uint16_t* deg, uint32_t v) {
     uint32_t* w = reinterpret_cast<uint32_t*>(deg) + (v >> 1);
-    atomicSub(w, 1u << ((v & 1) * 16));
+    const uint32_t sh = (v & 1) * 16;
+    return ((atomicSub(w, 1u << sh) >> sh) & 0xFFFFu) - 1u;
 }
 
-// Warp-aggregated append of `item` (when `pred`) to list[*count++].
+// Warp-aggregated append of `item` (when `pred`) to list[*count++]. Warp-uniform call sites only.
 __device__ __forceinline__ void append(bool pred, uint32_t item, uint32_t* list, uint32_t* count) {
     const unsigned b = __ballot_sync(FULL, pred);
     if (!b) return;
     const int lane = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
     uint32_t base = 0;
-    if (lane == __ffs(b) - 1) base = atomicAdd(count, (uint32_t)__popc(b));
-    base = __shfl_sync(FULL, base, __ffs(b) - 1);
+    if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(b));
+    base = __shfl_sync(FULL, base, leader);
     if (pred) list[base + __popc(b & ((1u << lane) - 1u))] = item;
 }
 
@@ -107,7 +112,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, SpShared& s) {
     return s.red[0];
 }
 
-// Exclusive block scan of x over 1024 threads; returns the exclusive prefix, total via ref.
+// Exclusive block scan of x over 1024 threads; `total` receives the sum.
 __device__ __forceinline__ uint32_t block_exscan(uint32_t x, uint32_t& total, SpShared& s) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t inc = x;
@@ -120,13 +125,14 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t x, uint32_t& total, Sp
     if (lane == 31) s.red[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-        uint32_t t = s.red[lane], ti = t;
+        const uint32_t t = s.red[lane];
+        uint32_t ti = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(FULL, ti, o);
             if (lane >= o) ti += y;
         }
-        s.red[lane] = ti - t;  // exclusive warp offsets
+        s.red[lane] = ti - t;
         if (lane == 31) s.scan_total = ti;
     }
     __syncthreads();
@@ -138,30 +144,26 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t x, uint32_t& total, Sp
 
 // ---------------------------------------------------------------- the node of one CTA
 
-template <bool INSTR>
 struct CtaNode {
     uint16_t* deg;        // smem, npad entries
     uint32_t* cbuf;       // smem, SP_THREADS: chunk vertices
     uint32_t* cstart;     // smem, SP_THREADS + 1: chunk prefix offsets
     SpShared* sh;
     const SparseArgs* a;
-    uint32_t* L1;         // global scratch lists (n each)
-    uint32_t* L2;
-    uint32_t* L3;
-    uint32_t* RL;         // removal list (claimed vertices)
-    uint32_t* T;          // triangle proposers
-    uint32_t* P;          // their partners (2 per proposer)
-    uint32_t* cnt;        // per-vertex counters, all zero between uses
+    uint32_t *A1, *A2, *N1, *N2;  // candidate lists: this round (A) and the next (N)
+    uint32_t *L3, *RL, *T, *P;    // above-limit list, removal list, triangle proposers/partners
+    uint32_t* cnt;
     unsigned long long* owner;
     uint32_t* tag;
     uint32_t epoch;
+    bool fresh;           // the candidate lists describe the current degrees
 
-    // Full scan: degree-one / degree-two / above-limit candidate lists, alive degree sum and
-    // the max-degree key (degree << 32 | ~id: smallest id wins ties).
+    // Full scan. With `lists`, rebuilds A1 (degree one), A2 (degree two) and L3 (above lim);
+    // always: alive degree sum (|E| = sum / 2) and the max-degree key (degree << 32 | ~id).
     __device__ void scan(uint32_t lim, bool lists) {
         SpShared& s = *sh;
         if (threadIdx.x == 0) {
-            s.c1 = s.c2 = s.cH = 0;
+            if (lists) s.a1 = s.a2 = s.cH = 0;
             s.sumdeg = 0;
             s.maxkey = 0;
         }
@@ -169,23 +171,32 @@ struct CtaNode {
         uint32_t sum = 0;
         unsigned long long mk = 0;
         const uint32_t n = a->n;
-        for (uint32_t base = 0; base < n; base += 2 * SP_THREADS) {
-            const uint32_t v0 = base + 2 * threadIdx.x;
-            uint32_t pair = v0 < n ? reinterpret_cast<const uint32_t*>(deg)[v0 >> 1] : 0xFFFFFFFFu;
+        const uint4* d4 = reinterpret_cast<const uint4*>(deg);
+        for (uint32_t base = 0; base < a->npad; base += 8 * SP_THREADS) {
+            const uint32_t v0 = base + 8 * threadIdx.x;
+            const uint4 q = v0 < a->npad ? d4[v0 >> 3] : make_uint4(FULL, FULL, FULL, FULL);
+            bool any = false;
+            uint32_t cand1 = 0, cand2 = 0, candH = 0;  // bit h: element h is a candidate
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 8; ++h) {
+                const uint32_t d = (comp(q, h >> 1) >> (16 * (h & 1))) & 0xFFFFu;
                 const uint32_t v = v0 + h;
-                const uint32_t d = (pair >> (16 * h)) & 0xFFFFu;
-                const bool al = v < n && d != DREM;
-                if (al) {
+                if (d != DREM && v < n) {
                     sum += d;
                     const unsigned long long key = ((unsigned long long)d << 32) | (0xFFFFFFFFu - v);
                     mk = key > mk ? key : mk;
+                    cand1 |= (d == 1) << h;
+                    cand2 |= (d == 2) << h;
+                    candH |= (d > lim) << h;
                 }
-                if (lists) {
-                    append(al && d == 1, v, L1, &s.c1);
-                    append(al && d == 2, v, L2, &s.c2);
-                    append(al && d > lim, v, L3, &s.cH);
+            }
+            any = lists && (cand1 | cand2 | candH);
+            if (__any_sync(FULL, any)) {
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    append((cand1 >> h) & 1u, v0 + h, A1, &s.a1);
+                    append((cand2 >> h) & 1u, v0 + h, A2, &s.a2);
+                    append((candH >> h) & 1u, v0 + h, L3, &s.cH);
                 }
             }
         }
@@ -200,12 +211,16 @@ struct CtaNode {
             atomicMax(&s.maxkey, mk);
         }
         __syncthreads();
-        if (threadIdx.x == 0) s.edges = (uint32_t)(s.sumdeg / 2);
+        if (threadIdx.x == 0) {
+            s.edges = (uint32_t)(s.sumdeg / 2);
+            s.maxdeg = (uint32_t)(s.maxkey >> 32);
+        }
         __syncthreads();
     }
 
-    // Decrement the alive neighbours of every vertex of list[0..count) (already claimed),
-    // load-balanced over the neighbour slices with a block scan (merge-path style).
+    // f(valid, u, w) for every (u in list, w in N(u)), load-balanced over the neighbour slices
+    // (block scan of the slice lengths, then a binary search per item). Every thread runs the
+    // same number of iterations, so f may use warp collectives.
     template <class F>
     __device__ void for_each_neighbor(const uint32_t* list, uint32_t count, F f) {
         SpShared& s = *sh;
@@ -217,30 +232,58 @@ struct CtaNode {
             const uint32_t st = block_exscan(dg, total, s);
             cbuf[threadIdx.x] = u;
             cstart[threadIdx.x] = st;
-            if (threadIdx.x == 0) cstart[SP_THREADS] = total;
             __syncthreads();
             const uint32_t items = min(count - base, SP_THREADS);
-            for (uint32_t idx = threadIdx.x; idx < total; idx += SP_THREADS) {
-                // last j with cstart[j] <= idx
-                uint32_t lo = 0, hi = items - 1;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi + 1) >> 1;
-                    if (cstart[mid] <= idx) lo = mid;
-                    else hi = mid - 1;
+            for (uint32_t ib = 0; ib < total; ib += SP_THREADS) {
+                const uint32_t idx = ib + threadIdx.x;
+                const bool valid = idx < total;
+                uint32_t uu = 0, w = 0;
+                if (valid) {
+                    uint32_t lo = 0, hi = items - 1;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi + 1) >> 1;
+                        if (cstart[mid] <= idx) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    uu = cbuf[lo];
+                    w = a->nbr[a->off[uu] + (idx - cstart[lo])];
                 }
-                const uint32_t uu = cbuf[lo];
-                f(uu, a->nbr[a->off[uu] + (idx - cstart[lo])]);
+                f(valid, uu, w);
             }
             __syncthreads();
         }
     }
 
-    __device__ void remove_claimed(uint32_t count) {
+    // Decrement the alive neighbours of the claimed RL[0..count) (all tagged with `ep`);
+    // vertices whose degree drops to 1 / 2 join the candidate lists `to1` / `to2`; |E| and |S|
+    // are updated (edges to alive neighbours + edges inside RL, counted once).
+    __device__ void remove_claimed(uint32_t count, uint32_t ep, uint32_t* to1, uint32_t* c1,
+                                   uint32_t* to2, uint32_t* c2) {
+        SpShared& s = *sh;
         uint16_t* dg = deg;
-        for_each_neighbor(RL, count, [dg](uint32_t, uint32_t w) {
-            if (dg[w] != DREM) ddec(dg, w);
+        const uint32_t* tg = tag;
+        uint32_t cut = 0;
+        for_each_neighbor(RL, count, [&](bool valid, uint32_t u, uint32_t w) {
+            uint32_t nd = 0xFFFFu;
+            if (valid) {
+                if (dg[w] != DREM) {
+                    nd = ddec(dg, w);
+                    ++cut;
+                } else if (tg[w] == ep && w > u) {
+                    ++cut;
+                }
+            }
+            append(nd == 1, w, to1, c1);
+            append(nd == 2, w, to2, c2);
         });
-        if (threadIdx.x == 0) sh->cc += count;
+        cut = __reduce_add_sync(FULL, cut);
+        if ((threadIdx.x & 31) == 0 && cut) atomicAdd(&s.ecut, cut);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s.cc += count;
+            s.edges -= s.ecut;
+            s.ecut = 0;
+        }
         __syncthreads();
     }
 
@@ -262,75 +305,90 @@ struct CtaNode {
         return lo < end && a->nbr[lo] == key;
     }
 
-    // Returns the number of vertices this phase put into the cover.
+    // claim u (if still alive) into RL, tagged with the phase epoch
+    __device__ __forceinline__ void claim_into_rl(bool want, uint32_t u, uint32_t ep) {
+        const bool got = want && dclaim(deg, u) != DREM;
+        if (got) tag[u] = ep;
+        append(got, u, RL, &sh->nrem);
+    }
+
+    // degree one over A1 (entries whose degree is still 1); new degree-1 vertices go to N1
+    // (next round), new degree-2 ones to A2 (this round's degree-two phase)
     __device__ uint32_t phase_degree_one() {
         SpShared& s = *sh;
-        const uint32_t c1 = s.c1;
+        const uint32_t c = s.a1;
+        const uint32_t ep = ++epoch;
         if (threadIdx.x == 0) s.nrem = 0;
         __syncthreads();
-        for (uint32_t base = 0; base < c1; base += SP_THREADS) {
+        for (uint32_t base = 0; base < c; base += SP_THREADS) {
             const uint32_t i = base + threadIdx.x;
             bool take = false;
             uint32_t u = 0;
-            if (i < c1) {
-                const uint32_t v = L1[i];
-                for (uint32_t e = a->off[v]; e < a->off[v + 1]; ++e) {
-                    const uint32_t w = a->nbr[e];
-                    if (deg[w] != DREM) {
-                        u = w;
-                        take = true;
-                        break;
+            if (i < c) {
+                const uint32_t v = A1[i];
+                if (deg[v] == 1) {
+                    for (uint32_t e = a->off[v]; e < a->off[v + 1]; ++e) {
+                        const uint32_t w = a->nbr[e];
+                        if (deg[w] != DREM) {
+                            u = w;
+                            take = true;
+                            break;
+                        }
                     }
+                    // isolated edge: the smaller id acts (reductions.cpp:7-19 visits it first)
+                    if (take && deg[u] == 1 && u < v) take = false;
                 }
-                // isolated edge: the smaller id acts (reductions.cpp:7-19 visits it first)
-                if (take && deg[u] == 1 && u < v) take = false;
-                if (take) take = dclaim(deg, u) != DREM;
             }
-            append(take, u, RL, &s.nrem);
+            claim_into_rl(take, u, ep);
         }
         __syncthreads();
         const uint32_t nrem = s.nrem;
-        if (nrem) remove_claimed(nrem);
+        if (nrem) remove_claimed(nrem, ep, N1, &s.n1, A2, &s.a2);
         return nrem;
     }
 
+    // degree two over A2 (entries whose degree is still 2); new candidates go to N1 / N2
     __device__ uint32_t phase_degree_two() {
         SpShared& s = *sh;
-        const uint32_t c2 = s.c2;
-        ++epoch;
-        const unsigned long long ep = (unsigned long long)(~epoch) << 32;
-        if (threadIdx.x == 0) s.nT = 0;
+        const uint32_t c = s.a2;
+        const uint32_t ep = ++epoch;
+        const unsigned long long key_hi = (unsigned long long)(~ep) << 32;
+        if (threadIdx.x == 0) {
+            s.nT = 0;
+            s.nrem = 0;
+        }
         __syncthreads();
-        // propose triangles (T: proposers, P: their partners)
-        for (uint32_t base = 0; base < c2; base += SP_THREADS) {
+        for (uint32_t base = 0; base < c; base += SP_THREADS) {
             const uint32_t i = base + threadIdx.x;
             bool tri = false;
             uint32_t v = 0, p0 = 0, p1 = 0;
-            if (i < c2) {
-                v = L2[i];
-                int f = 0;
-                for (uint32_t e = a->off[v]; e < a->off[v + 1] && f < 2; ++e) {
-                    const uint32_t w = a->nbr[e];
-                    if (deg[w] != DREM) {
-                        if (f == 0) p0 = w;
-                        else p1 = w;
-                        ++f;
+            if (i < c) {
+                v = A2[i];
+                if (deg[v] == 2) {
+                    int f = 0;
+                    for (uint32_t e = a->off[v]; e < a->off[v + 1] && f < 2; ++e) {
+                        const uint32_t w = a->nbr[e];
+                        if (deg[w] != DREM) {
+                            if (f == 0) p0 = w;
+                            else p1 = w;
+                            ++f;
+                        }
                     }
-                }
-                tri = f == 2 && has_edge(p0, p1);
-                if (tri) {
-                    const unsigned long long key = ep | v;
-                    atomicMin(owner + v, key);
-                    atomicMin(owner + p0, key);
-                    atomicMin(owner + p1, key);
+                    tri = f == 2 && has_edge(p0, p1);
+                    if (tri) {
+                        const unsigned long long key = key_hi | v;
+                        atomicMin(owner + v, key);
+                        atomicMin(owner + p0, key);
+                        atomicMin(owner + p1, key);
+                    }
                 }
             }
             const unsigned b = __ballot_sync(FULL, tri);
-            const int lane = threadIdx.x & 31;
-            uint32_t slot = 0;
             if (b) {
-                if (lane == __ffs(b) - 1) slot = atomicAdd(&s.nT, (uint32_t)__popc(b));
-                slot = __shfl_sync(FULL, slot, __ffs(b) - 1) + __popc(b & ((1u << lane) - 1u));
+                const int lane = threadIdx.x & 31, leader = __ffs(b) - 1;
+                uint32_t slot = 0;
+                if (lane == leader) slot = atomicAdd(&s.nT, (uint32_t)__popc(b));
+                slot = __shfl_sync(FULL, slot, leader) + __popc(b & ((1u << lane) - 1u));
                 if (tri) {
                     T[slot] = v;
                     P[2 * slot] = p0;
@@ -340,47 +398,48 @@ struct CtaNode {
         }
         __syncthreads();
         const uint32_t nT = s.nT;
-        if (threadIdx.x == 0) s.nrem = 0;
-        __syncthreads();
-        // vertex-disjoint winners remove both partners
+        // the smallest proposer of overlapping triangles acts: winners are vertex-disjoint
         for (uint32_t base = 0; base < nT; base += SP_THREADS) {
             const uint32_t i = base + threadIdx.x;
             bool win = false;
-            uint32_t p0 = 0, p1 = 0;
+            uint32_t v = 0, p0 = 0, p1 = 0;
             if (i < nT) {
-                const uint32_t v = T[i];
+                v = T[i];
                 p0 = P[2 * i];
                 p1 = P[2 * i + 1];
-                const unsigned long long key = ep | v;
+                const unsigned long long key = key_hi | v;
                 win = owner[v] == key && owner[p0] == key && owner[p1] == key;
             }
-            const bool c0 = win && dclaim(deg, p0) != DREM;
-            const bool c1 = win && dclaim(deg, p1) != DREM;
-            append(c0, p0, RL, &s.nrem);
-            append(c1, p1, RL, &s.nrem);
+            claim_into_rl(win, p0, ep);
+            claim_into_rl(win, p1, ep);
+            // a losing proposer whose triangle survives untouched must be tried again
+            append(i < nT && !win, v, N2, &s.n2);
         }
         __syncthreads();
         const uint32_t nrem = s.nrem;
-        if (nrem) remove_claimed(nrem);
+        if (nrem) remove_claimed(nrem, ep, N1, &s.n1, N2, &s.n2);
         return nrem;
     }
 
+    // high degree over L3 (from a fresh scan)
     __device__ uint32_t phase_high(uint32_t lim) {
         SpShared& s = *sh;
-        const uint32_t cH = s.cH;
-        if (cH > lim) {  // every one of them would enter S: |S| passes the bound
+        const uint32_t c = s.cH;
+        if (c > lim) {  // every one of them would enter S: |S| passes the bound
             if (threadIdx.x == 0) s.doom = 1;
             __syncthreads();
             return 0;
         }
-        for (uint32_t i = threadIdx.x; i < cH; i += SP_THREADS) {
+        const uint32_t ep = ++epoch;
+        for (uint32_t i = threadIdx.x; i < c; i += SP_THREADS) {
             const uint32_t u = L3[i];
             (void)dclaim(deg, u);
+            tag[u] = ep;
             RL[i] = u;
         }
         __syncthreads();
-        remove_claimed(cH);
-        return cH;
+        remove_claimed(c, ep, N1, &s.n1, N2, &s.n2);
+        return c;
     }
 
     __device__ bool doomed(uint32_t snap) const {
@@ -392,35 +451,52 @@ struct CtaNode {
     template <class Cnt>
     __device__ void reduce(uint32_t snap, Cnt& st) {
         SpShared& s = *sh;
+        if (!fresh) scan(limit_for(a->pvc, a->k, snap, s.cc), true);
         while (true) {
-            uint32_t lim = limit_for(a->pvc, a->k, snap, s.cc);
-            scan(lim, true);
             if (s.edges == 0) break;
+            const uint32_t lim = limit_for(a->pvc, a->k, snap, s.cc);
+            const bool high = s.maxdeg > lim;  // an upper bound: degrees only decrease
+            if (s.a1 == 0 && s.a2 == 0 && !high) break;  // no rule can fire
             ++st.rounds;
-            if (s.c1 == 0 && s.c2 == 0 && s.cH == 0) break;  // no rule can fire
+            if (threadIdx.x == 0) s.n1 = s.n2 = 0;
+            __syncthreads();
             bool changed = false;
-            if (s.c1) {
+            if (s.a1) {
                 const uint32_t r = phase_degree_one();
                 st.rm1 += r;
                 changed |= r != 0;
                 if (doomed(snap)) return;
-                if (r) scan(limit_for(a->pvc, a->k, snap, s.cc), true);
             }
-            if (s.c2 && s.edges) {
+            if (s.a2 && s.edges) {
                 const uint32_t r = phase_degree_two();
                 st.rm2 += r;
                 changed |= r != 0;
                 if (doomed(snap)) return;
-                if (r) scan(limit_for(a->pvc, a->k, snap, s.cc), true);
             }
-            lim = limit_for(a->pvc, a->k, snap, s.cc);
-            if (s.cH && s.edges) {
-                const uint32_t r = phase_high(lim);
+            bool rescan = false;
+            const uint32_t lim2 = limit_for(a->pvc, a->k, snap, s.cc);
+            if (s.maxdeg > lim2 && s.edges) {
+                scan(lim2, true);  // the above-limit list needs the current degrees
+                const uint32_t r = phase_high(lim2);
                 st.rmh += r;
                 changed |= r != 0;
                 if (doomed(snap)) return;
+                rescan = r != 0;  // the scan's A1/A2 predate these removals
             }
-            if (!changed) break;  // the last scan saw no applicable rule
+            if (rescan) {
+                scan(limit_for(a->pvc, a->k, snap, s.cc), true);
+            } else {
+                // next round's candidates: what this round's decrements produced
+                uint32_t* t;
+                t = A1; A1 = N1; N1 = t;
+                t = A2; A2 = N2; N2 = t;
+                if (threadIdx.x == 0) {
+                    s.a1 = s.n1;
+                    s.a2 = s.n2;
+                }
+                __syncthreads();
+            }
+            if (!changed) break;
         }
     }
 
@@ -435,6 +511,7 @@ struct CtaNode {
             sh->edges = h.y;
             sh->doom = 0;
         }
+        fresh = false;
         __syncthreads();
     }
     __device__ void copy_record(const unsigned char* src, unsigned char* dst) const {
@@ -449,22 +526,21 @@ struct CtaNode {
     // alive, and subtract from each affected survivor w its number of neighbours in X.
     __device__ void write_child(uint32_t v, unsigned char* rec) {
         SpShared& s = *sh;
-        ++epoch;
+        const uint32_t ep = ++epoch;
         if (threadIdx.x == 0) {
             s.nX = 0;
             s.nA = 0;
             s.eX = 0;
-            s.sumX = 0;
         }
         __syncthreads();
-        // X (in L1), tagged with the epoch
+        // X (in RL), tagged with the epoch
         const uint32_t b0 = a->off[v], b1 = a->off[v + 1];
         for (uint32_t base = b0; base < b1; base += SP_THREADS) {
             const uint32_t e = base + threadIdx.x;
             const uint32_t w = e < b1 ? a->nbr[e] : 0u;
             const bool al = e < b1 && deg[w] != DREM;
-            if (al) tag[w] = epoch;
-            append(al, w, L1, &s.nX);
+            if (al) tag[w] = ep;
+            append(al, w, RL, &s.nX);
         }
         // bulk copy of the parent's degrees
         uint4* d4 = reinterpret_cast<uint4*>(rec + 16);
@@ -475,7 +551,7 @@ struct CtaNode {
         uint16_t* rd = reinterpret_cast<uint16_t*>(rec + 16);
         uint32_t sx = 0;
         for (uint32_t i = threadIdx.x; i < nX; i += SP_THREADS) {
-            const uint32_t u = L1[i];
+            const uint32_t u = RL[i];
             sx += deg[u];
             rd[u] = DREM;
         }
@@ -484,21 +560,22 @@ struct CtaNode {
         const uint16_t* dg = deg;
         uint32_t* tg = tag;
         uint32_t* ct = cnt;
-        uint32_t* LA = L2;
-        uint32_t* nA = &s.nA;
-        uint32_t* eX = &s.eX;
-        const uint32_t ep = epoch;
-        for_each_neighbor(L1, nX, [dg, tg, ct, LA, nA, eX, ep](uint32_t u, uint32_t w) {
-            if (dg[w] == DREM) return;
-            if (tg[w] == ep) {
-                if (w > u) atomicAdd(eX, 1u);
-                return;
+        uint32_t* LA = A1;  // free after the reduction
+        uint32_t ex = 0;
+        for_each_neighbor(RL, nX, [&](bool valid, uint32_t u, uint32_t w) {
+            bool first = false;
+            if (valid && dg[w] != DREM) {
+                if (tg[w] == ep) ex += w > u;
+                else first = atomicAdd(ct + w, 1u) == 0u;
             }
-            if (atomicAdd(ct + w, 1u) == 0u) LA[atomicAdd(nA, 1u)] = w;
+            append(first, w, LA, &s.nA);
         });
+        ex = __reduce_add_sync(FULL, ex);
+        if ((threadIdx.x & 31) == 0 && ex) atomicAdd(&s.eX, ex);
+        __syncthreads();
         const uint32_t na = s.nA;
         for (uint32_t i = threadIdx.x; i < na; i += SP_THREADS) {
-            const uint32_t w = L2[i];
+            const uint32_t w = LA[i];
             rd[w] = (uint16_t)(deg[w] - cnt[w]);
             cnt[w] = 0;
         }
@@ -510,15 +587,21 @@ struct CtaNode {
         __syncthreads();
     }
 
-    // search_node.cpp:16-25 for one vertex (the remove-v branch)
-    __device__ void remove_one(uint32_t v) {
+    // search_node.cpp:16-25 for the branch vertex (the remove-v child); its decrements seed
+    // the child's candidate lists, so its reduction needs no opening scan.
+    __device__ void remove_branch_vertex(uint32_t v) {
+        SpShared& s = *sh;
+        const uint32_t ep = ++epoch;
         if (threadIdx.x == 0) {
             (void)dclaim(deg, v);
+            tag[v] = ep;
             RL[0] = v;
+            s.a1 = s.a2 = 0;
+            s.doom = 0;
         }
         __syncthreads();
-        remove_claimed(1);
-        // edges: recomputed by the next scan
+        remove_claimed(1, ep, A1, &s.a1, A2, &s.a2);
+        fresh = true;  // maxdeg from the closing scan stays a valid upper bound
     }
 };
 
@@ -530,23 +613,27 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
     if (worker >= a.workers) return;
     const int tid = threadIdx.x;
 
-    CtaNode<INSTR> x;
+    CtaNode x;
     x.deg = reinterpret_cast<uint16_t*>(smem4);
     x.cbuf = reinterpret_cast<uint32_t*>(x.deg + a.npad);
     x.cstart = x.cbuf + SP_THREADS;
     x.sh = &sh;
     x.a = &a;
-    uint32_t* scr = a.scratch + (unsigned long long)worker * 8ull * a.n;
-    x.L1 = scr;
-    x.L2 = scr + a.n;
-    x.L3 = scr + 2ull * a.n;
-    x.RL = scr + 3ull * a.n;
-    x.T = scr + 4ull * a.n;
-    x.cnt = scr + 5ull * a.n;
-    x.P = scr + 6ull * a.n;
+    uint32_t* scr = a.scratch + (unsigned long long)worker * 10ull * a.n;
+    x.A1 = scr;
+    x.A2 = scr + 1ull * a.n;
+    x.N1 = scr + 2ull * a.n;
+    x.N2 = scr + 3ull * a.n;
+    x.L3 = scr + 4ull * a.n;
+    x.RL = scr + 5ull * a.n;
+    x.T = scr + 6ull * a.n;
+    x.P = scr + 7ull * a.n;  // 2n
+    x.cnt = a.cnt + (unsigned long long)worker * a.n;
     x.owner = a.owner + (unsigned long long)worker * a.n;
     x.tag = a.tag + (unsigned long long)worker * a.n;
     x.epoch = 0;
+    x.fresh = false;
+    if (tid == 0) sh.ecut = 0;
 
     const unsigned long long t_start = globaltimer();
     const long long c_start = clock64();
@@ -570,6 +657,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
                 --sp;
                 x.load_record(slot_at(sp));
             } else {
+                // GlobalWorklist::remove_or_done: ticket, then publication / termination / cancel
                 if (tid == 0) {
                     if (!idle) atomicAdd(&ctl->work, ~ONE_PENDING + 1ull);
                     const unsigned long long pos = atomicAdd(&ctl->head, 1ull);
@@ -607,14 +695,14 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             have = true;
         }
 
-        // control line, node counter, limits
+        // control line, node counter, limits (thread 0), broadcast through shared memory
+        ++st.nodes;
         if (tid == 0) {
             const uint4 h = ld_volatile_v4(ctl);
             sh.red[0] = h.y;
             sh.red[1] = h.x;
             sh.red[2] = (uint32_t)ld_relaxed_u64(&ctl->work);
             int stop = 0;
-            ++st.nodes;
             if (st.nodes - nodes_flushed >= a.flush_every) {
                 const unsigned long long tot =
                     atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed) + (st.nodes - nodes_flushed);
@@ -628,8 +716,6 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
                 if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
             }
             sh.red[3] = stop;
-        } else {
-            ++st.nodes;
         }
         __syncthreads();
         const uint32_t cancel = sh.red[0], hbest = sh.red[1], qsize = sh.red[2], stop = sh.red[3];
@@ -680,20 +766,22 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             have = false;
             continue;
         }
-        // argmax from the last scan (smallest id among max degree)
+        // the smallest id among max-degree alive vertices (search_node.cpp:34-46)
+        x.scan(0xFFFFu, false);
         const uint32_t v = 0xFFFFFFFFu - (uint32_t)(sh.maxkey & 0xFFFFFFFFull);
         ++st.maxdeg;
 
-        // branch
+        // branch (scheduler.cpp:185-203)
         unsigned char* child = nullptr;
         unsigned long long* publish = nullptr;
         unsigned long long pos = 0;
         if (!a.seq_mode && qsize < a.threshold) {
             if (tid == 0) {
                 const unsigned long long old = atomicAdd(&ctl->work, ONE_PENDING | 1ull);
-                int ok = (uint32_t)old < a.capacity;
-                if (!ok) atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
-                else {
+                const int ok = (uint32_t)old < a.capacity;
+                if (!ok) {
+                    atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
+                } else {
                     st.max_queue = max(st.max_queue, (unsigned long long)((uint32_t)old + 1));
                     sh.pos = atomicAdd(&ctl->tail, 1ull);
                     unsigned long long* p = a.seq + (sh.pos & a.ring_mask);
@@ -718,7 +806,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             __syncthreads();
         }
         if (!child) {
-            if (sp >= a.stack_bound) {  // cannot happen within the provisioned depth
+            if (sp >= a.stack_bound) {  // deeper than the device-memory cap: fail loudly
                 if (tid == 0) {
                     atomicCAS(&ctl->status, 0, 3);
                     atomicExch(&ctl->cancel, 1u);
@@ -736,7 +824,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             if (tid == 0) st_release_u64(publish, pos + 1);
         }
         ++st.children;
-        x.remove_one(v);
+        x.remove_branch_vertex(v);
     }
 
     __syncthreads();
