@@ -290,16 +290,39 @@ struct Bits {
 };
 
 // A search node (degree array + counters) with the candidate sets the reference's ascending
-// rule passes query: deg==1 and deg==2 bitsets, and a lazy max-heap over (degree, -id).
+// rule passes and max_degree_vertex query. Degree buckets (one bitset per degree, O(1) moves)
+// give deg==1 / deg==2 find-next and the smallest-id max-degree vertex; when
+// (max degree + 1) x n/64 words would be too large, a lazy max-heap over (degree, -id) serves
+// the max-degree query instead.
 struct GreedyNode {
     const Graph& g;
     std::vector<uint32_t> deg;
     uint32_t cc = 0;
     uint64_t edges = 0;
-    Bits one, two;
-    std::priority_queue<uint64_t> heap;  // (deg << 32) | ~id : max degree, then smallest id
+    size_t words;
+    bool bucketed;
+    std::vector<uint64_t> bw;      // bucketed: (maxdeg + 1) x words
+    std::vector<uint32_t> bcount;  // alive vertices per degree
+    std::vector<size_t> bfirst;    // lowest possibly non-zero word per bucket
+    uint32_t maxd = 0;
+    Bits one, two;                 // heap mode only
+    Bits nt;                       // degree-two vertices already found not to be in a triangle
+    std::priority_queue<uint64_t> heap;  // heap mode: (deg << 32) | ~id
 
-    explicit GreedyNode(const Graph& G) : g(G), deg(G.n), one(G.n), two(G.n) {
+    explicit GreedyNode(const Graph& G)
+        : g(G), deg(G.n), words((size_t(G.n) + 63) / 64), one(0), two(0), nt(G.n) {
+        uint32_t md = 0;
+        for (uint32_t v = 0; v < g.n; ++v) md = std::max(md, g.degree(v));
+        bucketed = (size_t(md) + 1) * words <= (size_t(1) << 22);
+        if (bucketed) {
+            bw.assign((size_t(md) + 1) * words, 0);
+            bcount.assign(size_t(md) + 1, 0);
+            bfirst.assign(size_t(md) + 1, words);
+            maxd = md;
+        } else {
+            one = Bits(g.n);
+            two = Bits(g.n);
+        }
         for (uint32_t v = 0; v < g.n; ++v) {
             deg[v] = g.degree(v);
             track(v, kRemoved, deg[v]);
@@ -307,11 +330,38 @@ struct GreedyNode {
         edges = g.m;
     }
     void track(uint32_t v, uint32_t from, uint32_t to) {
+        if (to == 2) nt.clear(v);  // a new degree-two vertex has new partners: check it again
+        if (bucketed) {
+            const uint64_t bit = uint64_t(1) << (v & 63);
+            if (from != kRemoved) {
+                bw[size_t(from) * words + (v >> 6)] &= ~bit;
+                --bcount[from];
+            }
+            if (to != kRemoved) {
+                bw[size_t(to) * words + (v >> 6)] |= bit;
+                ++bcount[to];
+                bfirst[to] = std::min(bfirst[to], size_t(v >> 6));
+            }
+            return;
+        }
         if (from == 1) one.clear(v);
         if (from == 2) two.clear(v);
         if (to == 1) one.set(v);
         if (to == 2) two.set(v);
         if (to != kRemoved && to > 0) heap.push((uint64_t(to) << 32) | uint32_t(~v));
+    }
+    // first vertex >= from with degree d (d = 1 or 2), or UINT32_MAX
+    uint32_t next_with(uint32_t d, uint32_t from) {
+        if (!bucketed) return d == 1 ? one.next(from) : two.next(from);
+        if (d >= bcount.size() || from >= g.n) return UINT32_MAX;
+        const uint64_t* b = bw.data() + size_t(d) * words;
+        size_t k = from >> 6;
+        uint64_t x = b[k] & (~uint64_t(0) << (from & 63));
+        while (true) {
+            if (x) return uint32_t(k * 64 + __builtin_ctzll(x));
+            if (++k >= words) return UINT32_MAX;
+            x = b[k];
+        }
     }
     // search_node.cpp:16-25
     void remove(uint32_t v) {
@@ -336,23 +386,27 @@ struct GreedyNode {
     // reductions.cpp:7-19 (find-next on the live set == the ascending visit-time scan)
     bool degree_one() {
         bool changed = false;
-        for (uint32_t v = one.next(0); v != UINT32_MAX; v = v + 1 < g.n ? one.next(v + 1) : UINT32_MAX) {
+        for (uint32_t v = next_with(1, 0); v != UINT32_MAX; v = next_with(1, v + 1)) {
             uint64_t i = g.off[v];
-            uint32_t u = first_alive_neighbor(v, i);
-            remove(u);
+            remove(first_alive_neighbor(v, i));
             changed = true;
         }
         return changed;
     }
-    // reductions.cpp:22-40
+    // reductions.cpp:22-40. A degree-two vertex keeps its partners (and so its non-triangle
+    // verdict) until its degree changes, so verdicts are cached; the acting order is unchanged.
     bool degree_two_triangle() {
         bool changed = false;
-        for (uint32_t v = two.next(0); v != UINT32_MAX; v = v + 1 < g.n ? two.next(v + 1) : UINT32_MAX) {
+        for (uint32_t v = next_with(2, 0); v != UINT32_MAX; v = next_with(2, v + 1)) {
+            if ((nt.w[v >> 6] >> (v & 63)) & 1u) continue;
             uint64_t i = g.off[v];
             uint32_t a = first_alive_neighbor(v, i);
             ++i;
             uint32_t b = first_alive_neighbor(v, i);
-            if (!g.has_edge(a, b)) continue;
+            if (!g.has_edge(a, b)) {
+                nt.set(v);
+                continue;
+            }
             remove(a);
             remove(b);
             changed = true;
@@ -361,6 +415,14 @@ struct GreedyNode {
     }
     // search_node.cpp:34-46 (only queried while edges remain, so the max degree is >= 1)
     uint32_t max_degree_vertex() {
+        if (bucketed) {
+            while (bcount[maxd] == 0) --maxd;
+            const uint64_t* b = bw.data() + size_t(maxd) * words;
+            size_t k = bfirst[maxd];
+            while (!b[k]) ++k;
+            bfirst[maxd] = k;
+            return uint32_t(k * 64 + __builtin_ctzll(b[k]));
+        }
         while (true) {
             uint64_t top = heap.top();
             uint32_t v = ~uint32_t(top), d = uint32_t(top >> 32);
