@@ -191,8 +191,6 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         if (p->mode == VCG_PVC && p->k < 1) return fail(VCG_EINVAL, "pvc requires k >= 1");
         if (p->strategy < VCG_HYBRID || p->strategy > VCG_STACKONLY)
             return fail(VCG_EINVAL, "unknown strategy");
-        if (p->strategy == VCG_STACKONLY)
-            return fail(VCG_EINVAL, "the stackonly strategy is not available in this build");
         if (p->num_seeds && !p->seeds) return fail(VCG_EINVAL, "null seeds");
         const auto t0 = std::chrono::steady_clock::now();
         const bool pvc = p->mode == VCG_PVC;

@@ -325,8 +325,10 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     // idle back-off: exponential from 32 ns, capped at backoff_us (at most 2 us on the device —
     // a polling warp costs one L2 read, an over-sleeping one leaves queued work unclaimed)
     a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
-    a.seq_mode = s.strategy == 1 ? 1 : 0;
+    a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
     a.donate_oldest = s.donate_oldest ? 1 : 0;
+    a.stackonly = s.strategy == 2 ? 1 : 0;
+    a.depth = s.depth;
     a.mailbox = s.mailbox;
 
     CUDA_CHECK(cudaEventRecord(C.ev0, st));
@@ -353,6 +355,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     out.wl_current = (uint32_t)hc.work;
     out.wl_removed = hc.tail - out.wl_current;
     out.wl_max_size = nseeds;
+    if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
     out.worker_nodes.resize(workers);
     out.worker_high_water.resize(workers);
     for (uint32_t w = 0; w < workers; ++w) {
@@ -532,8 +535,10 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
     a.flush_every = s.node_budget ? 1 : 16;
     a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
-    a.seq_mode = s.strategy == 1 ? 1 : 0;
+    a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
     a.donate_oldest = s.donate_oldest ? 1 : 0;
+    a.stackonly = s.strategy == 2 ? 1 : 0;
+    a.depth = s.depth;
     a.mailbox = s.mailbox;
 
     CUDA_CHECK(cudaFuncSetAttribute(sparse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -558,6 +563,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     out.wl_current = (uint32_t)hc.work;
     out.wl_removed = hc.tail - out.wl_current;
     out.wl_max_size = nseeds;
+    if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
     out.worker_nodes.resize(workers);
     out.worker_high_water.resize(workers);
     for (uint32_t w = 0; w < workers; ++w) {

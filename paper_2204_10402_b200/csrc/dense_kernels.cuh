@@ -86,6 +86,8 @@ struct DenseArgs {
     uint32_t backoff_ns;
     int seq_mode;             // never donate (solve_*_seq semantics)
     int donate_oldest;        // donate the bottom (oldest) stacked node instead of the new child
+    int stackonly;            // StackOnly strategy (scheduler.cpp:214-297): claim sub-tree ids
+    uint32_t depth;           // StackOnly sub-tree depth (2^depth sub-trees)
     volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out,
                                  // [3] found out
 };
@@ -495,6 +497,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_k
         return my_stack + (unsigned long long)j * a.entry_bytes;
     };
     bool have = false, idle = true;
+    unsigned long long subtree = 0;  // StackOnly: current sub-tree id
+    uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
     unsigned long long nodes_flushed = 0;
 
@@ -508,6 +512,19 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_k
             if (sp > 0) {
                 --sp;
                 src = slot_at(sp);
+            } else if (a.stackonly) {
+                // stackonly_worker (scheduler.cpp:279-281): claim the next sub-tree id and
+                // replay its root path from the root record (ring slot 0, never consumed)
+                unsigned long long t = 0;
+                int o = 0;
+                if (lane == 0) {
+                    t = atomicAdd(&ctl->head, 1ull);
+                    o = (t >> a.depth) == 0 && !ld_volatile_v4(ctl).y;
+                }
+                if (!__shfl_sync(FULL, o, 0)) break;
+                subtree = __shfl_sync(FULL, t, 0);
+                replay = 0;
+                src = a.wl;
             } else {
                 // GlobalWorklist::remove_or_done (worklist.cpp:21-48): take a ticket, then wait
                 // for that slot's publication, for termination (pending == 0) or a cancel.
@@ -632,6 +649,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_k
         // below its threshold (with donate_oldest the oldest stacked node goes instead and the
         // child is stacked) — and continue with remove-v.
         long long tb = INSTR ? clock64() : 0;
+        // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
+        // child (0 = remove v_max, 1 = remove N(v_max), scheduler.cpp:303-309), nothing deferred
+        const bool replaying = a.stackonly && replay < a.depth;
+        const bool right = replaying && ((subtree >> replay) & 1ull);
+        replay += replaying;
         unsigned char* child = nullptr;
         unsigned long long* publish = nullptr;
         unsigned long long pos = 0;
@@ -664,19 +686,25 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_k
                 ++st.donated;
             }
         }
-        if (!child) {
-            child = slot_at(sp);
-            ++sp;
-            if (sp > st.high_water) st.high_water = sp;
+        if (!replaying || right) {
+            if (!child) {
+                child = slot_at(sp);
+                ++sp;
+                if (sp > st.high_water) st.high_water = sp;
+            }
+            x.write_child(xl, xcnt, child);
+            ++st.children;
         }
-        x.write_child(xl, xcnt, child);
-        ++st.children;
         if (publish) {
             __threadfence();
             __syncwarp();
             if (lane == 0) st_release_u64(publish, pos + 1);
         }
         if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
+        if (right) {  // replay continues with the remove-N(v) child just stacked
+            have = false;
+            continue;
+        }
         long long tv = INSTR ? clock64() : 0;
         x.remove_vertex(v);
         if (INSTR) st.phase[PH_BRANCH_V] += clock64() - tv;

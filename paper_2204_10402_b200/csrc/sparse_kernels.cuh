@@ -55,6 +55,8 @@ struct SparseArgs {
     unsigned long long node_budget, timeout_ns, flush_every;
     uint32_t backoff_ns;
     int seq_mode, donate_oldest;
+    int stackonly;            // StackOnly strategy (scheduler.cpp:214-297)
+    uint32_t depth;
     volatile uint32_t* mailbox;
 };
 
@@ -648,6 +650,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         return my_stack + (unsigned long long)j * a.entry_bytes;
     };
     bool have = false, idle = true;
+    unsigned long long subtree = 0;  // StackOnly: current sub-tree id
+    uint32_t replay = 0xFFFFFFFFu;   // StackOnly: root-path levels replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
     unsigned long long nodes_flushed = 0;
 
@@ -656,6 +660,18 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             if (sp > 0) {
                 --sp;
                 x.load_record(slot_at(sp));
+            } else if (a.stackonly) {
+                // stackonly_worker (scheduler.cpp:279-281): next sub-tree id, replay from the root
+                if (tid == 0) {
+                    const unsigned long long t = atomicAdd(&ctl->head, 1ull);
+                    sh.outcome = (t >> a.depth) == 0 && !ld_volatile_v4(ctl).y;
+                    sh.pos = t;
+                }
+                __syncthreads();
+                if (!sh.outcome) break;
+                subtree = sh.pos;
+                replay = 0;
+                x.load_record(a.wl);
             } else {
                 // GlobalWorklist::remove_or_done: ticket, then publication / termination / cancel
                 if (tid == 0) {
@@ -805,25 +821,35 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             }
             __syncthreads();
         }
-        if (!child) {
-            if (sp >= a.stack_bound) {  // deeper than the device-memory cap: fail loudly
-                if (tid == 0) {
-                    atomicCAS(&ctl->status, 0, 3);
-                    atomicExch(&ctl->cancel, 1u);
+        // StackOnly replay: bit `replay` of the sub-tree id picks the child, nothing deferred
+        const bool replaying = a.stackonly && replay < a.depth;
+        const bool right = replaying && ((subtree >> replay) & 1ull);
+        replay += replaying;
+        if (!replaying || right) {
+            if (!child) {
+                if (sp >= a.stack_bound) {  // deeper than the device-memory cap: fail loudly
+                    if (tid == 0) {
+                        atomicCAS(&ctl->status, 0, 3);
+                        atomicExch(&ctl->cancel, 1u);
+                    }
+                    break;
                 }
-                break;
+                child = slot_at(sp);
+                ++sp;
+                if (sp > st.high_water) st.high_water = sp;
             }
-            child = slot_at(sp);
-            ++sp;
-            if (sp > st.high_water) st.high_water = sp;
+            x.write_child(v, child);
+            ++st.children;
         }
-        x.write_child(v, child);
         if (publish) {
             __threadfence();
             __syncthreads();
             if (tid == 0) st_release_u64(publish, pos + 1);
         }
-        ++st.children;
+        if (right) {  // continue with the remove-N(v) child just stacked
+            have = false;
+            continue;
+        }
         x.remove_branch_vertex(v);
     }
 

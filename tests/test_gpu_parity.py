@@ -287,3 +287,41 @@ def test_c4_budgeted_run(config_golden):
     assert r["engine"] == 2 and r["status"] == "budget"
     assert r["size"] <= config_golden["c4"]["greedy"]
     check_cover(g, r)
+
+
+# ---- StackOnly (scheduler.cpp:214-297) ----------------------------------------------------
+
+@pytest.mark.parametrize("engine", ["dense", "sparse"])
+@pytest.mark.parametrize("workers,depth", [(1, 1), (4, 4), (8, 8)])
+def test_stackonly_corpus_exact(corpus, engine, workers, depth):
+    """acceptance_main.cpp:96-133 with run_stackonly: sizes equal the oracle's."""
+    bad = []
+    for it in corpus[::4]:
+        g = graph_of(it)
+        r = vc.solve_mvc(g, strategy="stackonly", workers=workers, depth=depth, engine=engine)
+        check_cover(g, r)
+        if r["size"] != it["mvc"] or r["status"] != "complete" or len(r["worker_nodes"]) != workers:
+            bad.append((it["name"], r["size"], it["mvc"]))
+        if r["worklist"]["added"] != 0:  # StackOnly reports empty worklist stats
+            bad.append((it["name"], "worklist"))
+    assert not bad, bad[:10]
+
+
+def test_stackonly_pvc_and_configs(config_golden):
+    g = load_config("c1")
+    r = vc.solve_mvc(g, strategy="stackonly", workers=64, depth=12)
+    assert r["size"] == config_golden["c1"]["mvc"]
+    check_cover(g, r)
+    assert not vc.solve_pvc(g, 84, strategy="stackonly", workers=64, depth=10)["feasible"]
+    y = vc.solve_pvc(g, 85, strategy="stackonly", workers=64, depth=10)
+    assert y["feasible"]
+    check_cover(g, y)
+
+
+def test_stackonly_load_imbalance_vs_hybrid(config_golden):
+    """The paper's Fig. 5 direction on C3: hybrid balances load better than StackOnly."""
+    g = load_config("c3")
+    so = vc.solve_mvc(g, strategy="stackonly", workers=256, depth=10)
+    hy = vc.solve_mvc(g, strategy="hybrid", workers=256)
+    assert so["size"] == hy["size"] == config_golden["c3"]["mvc"]
+    assert max(hy["load_ratios"]) < max(so["load_ratios"])
