@@ -164,6 +164,8 @@ struct WarpNode {
     uint32_t d[W];                   // degree of vertex 32*i + lane (meaningless once removed)
     uint32_t alv;                    // bit i: vertex 32*i + lane is alive (not in the cover)
     uint32_t aw;                     // lane j < W: alive bitmap word j (vertices 32j..32j+31)
+    uint32_t nt;                     // bit i: vertex 32*i + lane has degree two and was found
+                                     // not to close a triangle; valid until its degree changes
     uint32_t cc, edges;              // uniform
     bool doom;                       // uniform: proven to be pruned (see reduce)
     const uint4* sat;                // shared adjacency bitmap
@@ -188,12 +190,18 @@ struct WarpNode {
     __device__ __forceinline__ void remove_vertex(uint32_t u) {
         uint32_t du = lane < W ? __popc(row_word(u, lane) & aw) : 0u;
         du = __reduce_add_sync(FULL, du);
+        uint32_t touched = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint4 r = sat[q * npad + u];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) d[4 * q + c] -= (comp(r, c) >> lane) & 1u;
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t bit = (comp(r, c) >> lane) & 1u;
+                d[4 * q + c] -= bit;
+                touched |= bit << (4 * q + c);
+            }
         }
+        nt &= ~touched;  // a changed degree invalidates the cached non-triangle verdict
         if (lane == (int)(u & 31)) alv &= ~(1u << (u >> 5));
         if (lane == (int)(u >> 5)) aw &= ~(1u << (u & 31));
         cc += 1;
@@ -210,9 +218,10 @@ struct WarpNode {
         for (int i = 0; i < W; ++i) m |= (d[i] - lo <= span ? 1u : 0u) << i;
         return m & alv;
     }
-    __device__ __forceinline__ int find_first(int pos, uint32_t lo, uint32_t hi) const {
+    __device__ __forceinline__ int find_first(int pos, uint32_t lo, uint32_t hi,
+                                              uint32_t skip) const {
         const uint32_t pi = (uint32_t)pos >> 5;
-        uint32_t m = range_mask(lo, hi);
+        uint32_t m = range_mask(lo, hi) & ~skip;
         m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
         const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
         const uint32_t v = __reduce_min_sync(FULL, key);
@@ -239,7 +248,10 @@ struct WarpNode {
     __device__ __forceinline__ bool any_candidate(uint32_t lim) const {
         uint32_t m = 0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) m |= (d[i] - 1u <= 1u || d[i] > lim ? 1u : 0u) << i;
+        for (int i = 0; i < W; ++i) {
+            const bool two = d[i] == 2u && !((nt >> i) & 1u);
+            m |= (d[i] == 1u || two || d[i] > lim ? 1u : 0u) << i;
+        }
         return __any_sync(FULL, (m & alv) != 0);
     }
     // search_node.cpp:34-46: smallest id among alive vertices of maximum degree
@@ -282,7 +294,9 @@ struct WarpNode {
                 int pos = 0;
 #pragma unroll 1
                 while (!doomed(pvc, k, snap)) {
-                    const int v = find_first(pos, lo, hi);
+                    // (a degree-two vertex already known not to close a triangle is skipped:
+                    // its partners are unchanged while its degree is, so the test would fail)
+                    const int v = find_first(pos, lo, hi, pass == 2 ? nt : 0u);
                     if (v < 0) break;
                     pos = v + 1;
                     int u0 = v, u1 = -1;
@@ -294,6 +308,7 @@ struct WarpNode {
                             const bool tri = (row_word(p0, p1 >> 5) >> (p1 & 31)) & 1u;
                             u0 = tri ? p0 : -1;
                             u1 = tri ? p1 : -1;
+                            if (!tri && lane == (v & 31)) nt |= 1u << (v >> 5);
                         }
                     }
 #pragma unroll 1
@@ -421,6 +436,7 @@ struct WarpNode {
         cc = __shfl_sync(FULL, h.x, 0);
         edges = __shfl_sync(FULL, h.y, 0);
         doom = false;
+        nt = 0;
         alv = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
