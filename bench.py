@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--frontier-per-rank", type=int, default=1024)
+    ap.add_argument("--ref-sample-s", type=float, default=0.0,
+                    help="reference arm: seconds per bounded sample (0 = sized to the run)")
     return ap.parse_args()
 
 
@@ -141,7 +143,7 @@ def reference_line(args, rank, world):
     ref = Reference()
     g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
     cores = os.cpu_count() or 1
-    budget_s = max(2.0, min(12.0, 150.0 / max(1, args.steps + args.warmup)))
+    budget_s = args.ref_sample_s or max(2.0, min(12.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=1.0)
     rates, nodes = [], 0

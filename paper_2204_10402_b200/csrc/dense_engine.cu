@@ -116,6 +116,16 @@ __global__ void init_seq_kernel(unsigned long long* seq, uint32_t ring, uint32_t
         seq[i] = i < filled ? i + 1ull : (unsigned long long)i;
 }
 
+// dst[j] = src[idx[j]] for node records of `vec16` 16-byte vectors (frontier compaction)
+__global__ void gather_records_kernel(const unsigned char* src, const uint32_t* idx,
+                                      unsigned char* dst, uint32_t count, uint32_t vec16) {
+    for (uint32_t j = blockIdx.x; j < count; j += gridDim.x) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src) + (size_t)idx[j] * vec16;
+        uint4* d4 = reinterpret_cast<uint4*>(dst) + (size_t)j * vec16;
+        for (uint32_t t = threadIdx.x; t < vec16; t += blockDim.x) d4[t] = s4[t];
+    }
+}
+
 uint32_t pick_w(uint32_t n) {
     if (n <= 128) return 4;
     if (n <= 256) return 8;
@@ -622,24 +632,40 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
     const DeviceGraph& dg = *g.dev[dev];
     const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 * 33;  // see solve_on_device
 
-    // level 0: the root
-    std::vector<unsigned char> level(entry);
+    // Levels stay on the device: per level only the flags come down and the gather list of
+    // surviving children goes up; the final level is copied once.
+    struct DevBuf {
+        void* p = nullptr;
+        size_t bytes = 0;
+        void* get(size_t need) {
+            if (need > bytes) {
+                if (p) cudaFree(p);
+                p = nullptr;
+                CUDA_CHECK(cudaMalloc(&p, need));
+                bytes = need;
+            }
+            return p;
+        }
+        ~DevBuf() {
+            if (p) cudaFree(p);
+        }
+    } bin, bout, bflags, bcov, bidx;
     {
+        std::vector<unsigned char> root(entry);
         std::vector<uint32_t> deg(g.n);
         for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
-        pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), level.data());
+        pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), root.data());
+        CUDA_CHECK(cudaMemcpyAsync(bin.get(entry), root.data(), entry, cudaMemcpyHostToDevice, st));
     }
     uint64_t count = 1;
     f = Frontier();
     f.best = s.best;
+    std::vector<uint32_t> flags, covers, idx;
     while (count > 0 && count < target) {
-        unsigned char *din = nullptr, *dout = nullptr;
-        uint32_t *dflags = nullptr, *dcov = nullptr;
-        CUDA_CHECK(cudaMalloc(&din, count * entry));
-        CUDA_CHECK(cudaMalloc(&dout, 2 * count * entry));
-        CUDA_CHECK(cudaMalloc(&dflags, count * 4));
-        CUDA_CHECK(cudaMalloc(&dcov, count * (W + 1) * 4));
-        CUDA_CHECK(cudaMemcpyAsync(din, level.data(), count * entry, cudaMemcpyHostToDevice, st));
+        unsigned char* din = (unsigned char*)bin.p;
+        unsigned char* dout = (unsigned char*)bout.get(2 * count * entry);
+        uint32_t* dflags = (uint32_t*)bflags.get(count * 4);
+        uint32_t* dcov = (uint32_t*)bcov.get(count * (W + 1) * 4);
         ExpandArgs a;
         a.at4 = dg.at4;
         a.n = g.n;
@@ -667,45 +693,55 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
         }
         CUDA_CHECK(cudaGetLastError());
         ++f.launches;
-        std::vector<uint32_t> flags(count), covers(count * (W + 1));
-        std::vector<unsigned char> out(2 * count * entry);
+        flags.resize(count);
         CUDA_CHECK(cudaMemcpyAsync(flags.data(), dflags, count * 4, cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaMemcpyAsync(covers.data(), dcov, covers.size() * 4, cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaMemcpyAsync(out.data(), dout, out.size(), cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
-        cudaFree(din);
-        cudaFree(dout);
-        cudaFree(dflags);
-        cudaFree(dcov);
         f.nodes += count;
         ++f.levels;
         // covers found on this level (fixed bound inside the level, improved between levels)
-        for (uint64_t i = 0; i < count; ++i) {
-            if (flags[i] != 1) continue;
-            const uint32_t* c = &covers[i * (W + 1)];
-            if (s.pvc ? !f.found : c[0] < f.best) {
-                f.found = true;
-                if (!s.pvc) f.best = c[0];
-                f.cover.clear();
-                for (uint32_t v = 0; v < g.n; ++v)
-                    if ((c[1 + (v >> 5)] >> (v & 31)) & 1u) f.cover.push_back(v);
+        bool any_cover = false;
+        for (uint64_t i = 0; i < count; ++i) any_cover |= flags[i] == 1;
+        if (any_cover) {
+            covers.resize(count * (W + 1));
+            CUDA_CHECK(cudaMemcpy(covers.data(), dcov, covers.size() * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < count; ++i) {
+                if (flags[i] != 1) continue;
+                const uint32_t* c = &covers[i * (W + 1)];
+                if (s.pvc ? !f.found : c[0] < f.best) {
+                    f.found = true;
+                    if (!s.pvc) f.best = c[0];
+                    f.cover.clear();
+                    for (uint32_t v = 0; v < g.n; ++v)
+                        if ((c[1 + (v >> 5)] >> (v & 31)) & 1u) f.cover.push_back(v);
+                }
             }
         }
         if (s.pvc && f.found) {
             count = 0;
-            level.clear();
             break;
         }
-        std::vector<unsigned char> next;
-        next.reserve(2 * count * entry);
-        uint64_t nc = 0;
-        for (uint64_t i = 0; i < count; ++i) {
-            if (flags[i] != 2) continue;
-            next.insert(next.end(), out.begin() + (2 * i) * entry, out.begin() + (2 * i + 2) * entry);
-            nc += 2;
+        idx.clear();
+        for (uint64_t i = 0; i < count; ++i)
+            if (flags[i] == 2) {
+                idx.push_back((uint32_t)(2 * i));
+                idx.push_back((uint32_t)(2 * i + 1));
+            }
+        const uint64_t nc = idx.size();
+        if (nc) {
+            uint32_t* didx = (uint32_t*)bidx.get(nc * 4);
+            CUDA_CHECK(cudaMemcpyAsync(didx, idx.data(), nc * 4, cudaMemcpyHostToDevice, st));
+            unsigned char* dnext = (unsigned char*)bin.get(nc * entry);
+            gather_records_kernel<<<(uint32_t)std::min<uint64_t>(nc, 65535), 64, 0, st>>>(
+                dout, didx, dnext, (uint32_t)nc, (uint32_t)(entry / 16));
+            CUDA_CHECK(cudaGetLastError());
+            ++f.launches;
         }
-        level.swap(next);
         count = nc;
+    }
+    std::vector<unsigned char> level(count * entry);
+    if (count) {
+        CUDA_CHECK(cudaMemcpyAsync(level.data(), bin.p, count * entry, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
     }
     // unpack the frontier into [cc, edges, deg[n]] records
     f.records.assign(count * (2 + (size_t)g.n), 0);

@@ -481,7 +481,10 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
 // ------------------------------------------------------------------ the traversal kernel
 
 template <int W, bool INSTR>
-__global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? 2 : 1))) dense_kernel(DenseArgs a) {
+#ifndef VCG_MINB16
+#define VCG_MINB16 2  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#endif
+__global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))) dense_kernel(DenseArgs a) {
     extern __shared__ uint4 smem[];
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;

@@ -129,3 +129,45 @@ def test_mvc_bound_is_exchanged_and_minimum_wins():
     for rank in (0, 1):
         r = res[rank][0]
         assert r["size"] == 5 and r["cover"] == [1, 2, 3, 4, 5]
+
+
+def decided_expander(graph, mode, k, target, device=0, stream=None):
+    """The frontier expansion itself found a cover (PVC decided, or the MVC optimum)."""
+    seeds = np.zeros((0, 2 + N), np.uint32)
+    return dict(seeds=seeds, nodes=7, levels=2, best=3 if mode == "mvc" else k, greedy_size=5,
+                found=True, cover=[0, 2, 4], kernel_launches=2)
+
+
+def worker_decided(rank, world, port, mode, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_10402_b200.distributed import Mailbox, solve_distributed
+    calls = []
+
+    def solver(graph, **kw):
+        calls.append(1)
+        raise AssertionError("no share to search")
+
+    r = solve_distributed(FakeGraph(), mode, 4 if mode == "pvc" else 0, frontier_per_rank=5,
+                          expander=decided_expander, solver=solver,
+                          mailbox=Mailbox(pinned=False), period=0.001)
+    out.put((rank, r, {"calls": len(calls)}))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["pvc", "mvc"])
+def test_frontier_decides_without_search_on_three_ranks(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=worker_decided, args=(r, 3, port, mode, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(3)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, r, log in got:
+        assert log["calls"] == 0
+        assert r["feasible"] and r["size"] == 3 and r["cover"] == [0, 2, 4]
+        assert r["nodes_total"] == 7
