@@ -92,6 +92,9 @@ struct DeviceCtx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
+    // One solve at a time per device: the arenas, events and the graph's lazily built device
+    // copy are shared state (the reference harness is synchronous too).
+    std::mutex solve_mu;
 };
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
@@ -146,10 +149,14 @@ std::vector<uint32_t> build_bitmap(const Graph& g, uint32_t W, uint32_t npad) {
     return at;
 }
 
-// Pack one node record: [cc, edges, 0, 0] + lane-major u16 degrees.
+// Node record: [cc, edges, 0, 0] + lane-major u16 degrees (2W bytes per lane) + one word per
+// lane of cached degree-two non-triangle verdicts.
+size_t dense_record_bytes(uint32_t W) { return 16 + 64 * (size_t)W + 128; }
+
+// Pack one node record.
 void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint32_t* deg,
                  unsigned char* rec) {
-    std::memset(rec, 0, 16 + 64 * (size_t)W);
+    std::memset(rec, 0, dense_record_bytes(W));  // no cached verdicts (nt = 0)
     uint32_t* h = reinterpret_cast<uint32_t*>(rec);
     h[0] = cc;
     h[1] = edges;
@@ -214,11 +221,12 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (dev < 0 || dev >= ndev) throw std::invalid_argument("device ordinal out of range");
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
+    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
     cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
 
     const uint32_t W = pick_w(g.n);
     const uint32_t npad = 32 * W;
-    const size_t entry = 16 + 64 * (size_t)W;
+    const size_t entry = dense_record_bytes(W);
     out.engine = 1;
     out.degree_bytes = 2;
     out.n_padded = npad;
@@ -407,6 +415,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (2 * g.m >= (1ull << 32)) throw std::invalid_argument("graph too large for u32 CSR offsets");
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
+    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
     cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
 
     uint32_t maxdeg = 0;
@@ -613,10 +622,11 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
     if (device_count() == 0) throw std::runtime_error("CUDA error: no CUDA device visible");
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
+    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
     cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
     const uint32_t W = pick_w(g.n);
     const uint32_t npad = 32 * W;
-    const size_t entry = 16 + 64 * (size_t)W;
+    const size_t entry = dense_record_bytes(W);
     if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
     if (!g.dev[dev]) {
         auto dg = std::make_shared<DeviceGraph>();

@@ -11,8 +11,9 @@
 //    the degrees of vertices 32*i + l (i < W), u32, kRemoved = 0xFFFFFFFF;
 //  * the read-only graph is an adjacency bitmap staged once per CTA in shared memory, word j of
 //    vertex w's row at uint4 group (j/4)*npad + w (column-coalesced, row-broadcast);
-//  * deferred nodes are 16 + 64*W byte records: {cover_count, edge_count, 0, 0} then lane-major
-//    u16 degrees (lane l's W entries contiguous), in a per-warp stack in HBM or the device ring.
+//  * deferred nodes are 16 + 64*W + 128 byte records: {cover_count, edge_count, 0, 0}, lane-major
+//    u16 degrees (lane l's W entries contiguous), then one word per lane of cached degree-two
+//    non-triangle verdicts; they live in a per-warp stack in HBM or in the device ring.
 //
 // Instruction footprint matters more than instruction count here: with the rule code inlined
 // at every call site the W=16 kernel was 128 KB of SASS and 64% of warp stalls were
@@ -364,19 +365,25 @@ struct WarpNode {
             ss[i * 32 + lane] = s;
         }
         uint32_t packed[W / 2];
-        uint32_t esum = 0;
+        uint32_t esum = 0, changed = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const bool keep = (keepm >> i) & 1u;
-            const uint32_t nd = keep ? d[i] - ss[i * 32 + lane] : 0xFFFFu;  // own writes: no sync
+            const uint32_t lost = ss[i * 32 + lane];  // own writes: no sync needed
+            const uint32_t nd = keep ? d[i] - lost : 0xFFFFu;
             esum += keep ? nd : 0u;
+            changed |= (lost != 0u ? 1u : 0u) << i;
             if (i & 1) packed[i / 2] |= nd << 16;
             else packed[i / 2] = nd;
         }
         const uint32_t e2 = __reduce_add_sync(FULL, esum);
         if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc + xcnt, e2 / 2);
         store_degrees(rec, packed);
-        __syncwarp();
+        store_nt(rec, nt & keepm & ~changed);  // verdicts of survivors whose degree held
+    }
+    // The cached non-triangle verdicts travel with the record (one word per lane).
+    __device__ __forceinline__ void store_nt(unsigned char* rec, uint32_t m) const {
+        reinterpret_cast<uint32_t*>(rec + 16 + 64 * W)[lane] = m;
     }
     __device__ __forceinline__ void store_degrees(unsigned char* rec, const uint32_t* packed) const {
         unsigned char* p = rec + 16 + lane * (2 * W);
@@ -399,6 +406,7 @@ struct WarpNode {
         }
         if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc, edges);
         store_degrees(rec, packed);
+        store_nt(rec, nt);
     }
     // Moves one record between stack and worklist memory without unpacking it.
     __device__ __forceinline__ void copy_record(const unsigned char* src, unsigned char* dst) const {
@@ -411,6 +419,7 @@ struct WarpNode {
             for (int t = 0; t < W / 8; ++t)
                 reinterpret_cast<uint4*>(q)[t] = __ldcg(reinterpret_cast<const uint4*>(p) + t);
         }
+        store_nt(dst, __ldcg(reinterpret_cast<const uint32_t*>(src + 16 + 64 * W) + lane));
         if (lane == 0) *reinterpret_cast<uint4*>(dst) = __ldcg(reinterpret_cast<const uint4*>(src));
     }
     // Loads a record through L2 (it may come from another SM's worklist donation).
@@ -436,7 +445,7 @@ struct WarpNode {
         cc = __shfl_sync(FULL, h.x, 0);
         edges = __shfl_sync(FULL, h.y, 0);
         doom = false;
-        nt = 0;
+        nt = __ldcg(reinterpret_cast<const uint32_t*>(rec + 16 + 64 * W) + lane);
         alv = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
