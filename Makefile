@@ -15,7 +15,9 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 HDRS     := $(wildcard $(SRC)/*.hpp) $(wildcard $(SRC)/*.cuh) include/vcgpu.h
 OBJS     := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
-all: $(LIB) oracle
+CLI      := $(PKG)/bin/vcsolve
+
+all: $(LIB) $(CLI) oracle
 
 $(OBJ)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -29,11 +31,16 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@.tmp $(OBJS) -Xlinker --exclude-libs,ALL -Xlinker -Bsymbolic
 	mv $@.tmp $@
 
+# the reference CLI's drop-in (tools/main.cpp), linked against the C-ABI only
+$(CLI): $(PKG)/cli/vcsolve.cpp include/vcgpu.h $(LIB)
+	@mkdir -p $(PKG)/bin
+	$(HOSTCXX) -O2 -std=c++17 -Wall -Wextra -Iinclude $< -o $@ -L$(PKG) -lvcgpu -Wl,-rpath,'$$ORIGIN/..'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
