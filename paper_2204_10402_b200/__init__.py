@@ -249,15 +249,22 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
                        capacity, threshold_fraction, depth, out)
 
 
+def _array(ptr, count):
+    """A library-owned C array as a Python int list (one bulk copy, not per-element ctypes)."""
+    if count == 0 or not ptr:
+        return []
+    return np.ctypeslib.as_array(ptr, shape=(count,)).tolist()
+
+
 def _result_dict(r):
     nw = r.num_workers
     return dict(
         status=_n.STATUS_NAMES[r.status], size=int(r.size), feasible=bool(r.feasible),
         greedy_size=int(r.greedy_size),
-        cover=[int(r.cover[i]) for i in range(r.cover_len)],
+        cover=_array(r.cover, r.cover_len),
         cover_from_search=bool(r.cover_from_search), num_workers=nw,
-        worker_nodes=[int(r.worker_nodes[i]) for i in range(nw)],
-        worker_stack_high_water=[int(r.worker_stack_high_water[i]) for i in range(nw)],
+        worker_nodes=_array(r.worker_nodes, nw),
+        worker_stack_high_water=_array(r.worker_stack_high_water, nw),
         nodes_total=int(r.nodes_total),
         worklist=dict(added=int(r.wl_added), removed=int(r.wl_removed),
                       max_size=int(r.wl_max_size), current_size=int(r.wl_current_size)),

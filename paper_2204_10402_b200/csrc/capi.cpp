@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -195,11 +196,23 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         const auto t0 = std::chrono::steady_clock::now();
         const bool pvc = p->mode == VCG_PVC;
 
-        // greedy seed (scheduler.cpp:333-340), counted in wall_ms like the reference
-        vcg::Greedy greedy = vcg::greedy_approx(g);
-        const auto t1 = std::chrono::steady_clock::now();
-        out->greedy_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-        out->greedy_size = greedy.size;
+        // greedy seed (scheduler.cpp:333-340), counted in wall_ms like the reference. MVC needs
+        // it as the initial bound before the search starts; PVC only reports its size
+        // (best := k, stack bound min(k, n)), so there it runs on a host thread while the
+        // device searches.
+        auto run_greedy = [&g, out]() {
+            const auto a = std::chrono::steady_clock::now();
+            vcg::Greedy gr = vcg::greedy_approx(g);
+            out->greedy_ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+            return gr;
+        };
+        vcg::Greedy greedy;
+        std::future<vcg::Greedy> greedy_async;
+        if (pvc && g.n > 0)
+            greedy_async = std::async(std::launch::async, run_greedy);
+        else
+            greedy = run_greedy();
 
         vcg::SolveSpec s;
         s.pvc = pvc;
@@ -230,6 +243,12 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         s.stream = p->stream;
 
         vcg::SolveOut r;
+        struct Join {  // the greedy thread never outlives this call, even on a device error
+            std::future<vcg::Greedy>& f;
+            ~Join() {
+                if (f.valid()) f.wait();
+            }
+        } join{greedy_async};
         if (g.n == 0) {
             // no vertex: one root visit, nothing to branch on (MVC 0; PVC feasible, empty)
             r.worker_nodes.assign(1, 1);
@@ -239,6 +258,9 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         } else {
             vcg::solve_on_device(g, s, r);
         }
+
+        if (greedy_async.valid()) greedy = greedy_async.get();
+        out->greedy_size = greedy.size;
 
         // finish_run (scheduler.cpp:299-324): certificate in original ids
         const std::vector<uint32_t>* cov = nullptr;

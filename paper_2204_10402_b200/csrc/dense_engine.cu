@@ -87,10 +87,26 @@ struct Arena {
         return p;
     }
 };
+// Grow-only pinned host staging for the end-of-solve readback (one async copy, no pageable
+// bounce through the driver).
+struct PinnedArena {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) CUDA_CHECK(cudaFreeHost(p));
+            p = nullptr;
+            CUDA_CHECK(cudaHostAlloc(&p, need, cudaHostAllocDefault));
+            bytes = need;
+        }
+        return p;
+    }
+};
 struct DeviceCtx {
     Arena stacks, wl, seq, misc, scratch;
+    PinnedArena host;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t evh = nullptr, ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
     // One solve at a time per device: the arenas, events and the graph's lazily built device
     // copy are shared state (the reference harness is synchronous too).
@@ -106,6 +122,7 @@ DeviceCtx& ctx_for(int dev) {
         auto c = std::make_unique<DeviceCtx>();
         CUDA_CHECK(cudaSetDevice(dev));
         CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaEventCreate(&c->evh));
         CUDA_CHECK(cudaEventCreate(&c->ev0));
         CUDA_CHECK(cudaEventCreate(&c->ev1));
         CUDA_CHECK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
@@ -186,6 +203,48 @@ int occupancy(uint32_t block, size_t smem, bool instr) {
     return nb;
 }
 
+// Kernel done → control block + per-worker stats into pinned memory with one stream sync;
+// device_ms from the kernel's events, h2d_ms from the upload's.
+const WStats* finish_and_read(DeviceCtx& C, cudaStream_t st, const Ctl* ctl, const WStats* stats,
+                              uint32_t workers, Ctl& hc, SolveOut& out) {
+    CUDA_CHECK(cudaEventRecord(C.ev1, st));
+    const size_t sb = (size_t)workers * sizeof(WStats);
+    unsigned char* h = static_cast<unsigned char*>(C.host.get(256 + sb));
+    CUDA_CHECK(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(h + 256, stats, sb, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
+    out.device_ms = ms;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, C.evh, C.ev0));
+    out.h2d_ms = ms;
+    std::memcpy(&hc, h, sizeof(Ctl));
+    out.d2h_bytes += sizeof(Ctl) + sb;
+    return reinterpret_cast<const WStats*>(h + 256);
+}
+
+// Per-worker counters → the run totals (WorkerMetrics, metrics.hpp:28-41).
+void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
+    out.worker_nodes.resize(workers);
+    out.worker_high_water.resize(workers);
+    for (uint32_t w = 0; w < workers; ++w) {
+        out.worker_nodes[w] = hs[w].nodes;
+        out.worker_high_water[w] = hs[w].high_water;
+        out.rounds += hs[w].rounds;
+        out.maxdeg += hs[w].maxdeg;
+        out.children += hs[w].children;
+        out.removals += hs[w].rm1 + hs[w].rm2 + hs[w].rmh;
+        out.rm1 += hs[w].rm1;
+        out.rm2 += hs[w].rm2;
+        out.rmh += hs[w].rmh;
+        out.dooms += hs[w].dooms;
+        out.donated += hs[w].donated;
+        out.active_cycles += hs[w].active;
+        out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
+        for (int p = 0; p < 10; ++p) out.phase[p] += hs[w].phase[p];
+    }
+}
+
 }  // namespace
 
 uint32_t* mailbox_alloc(uint32_t n_words) {
@@ -231,7 +290,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     out.degree_bytes = 2;
     out.n_padded = npad;
 
-    auto th0 = std::chrono::steady_clock::now();
+    CUDA_CHECK(cudaEventRecord(C.evh, st));
     // resident graph (adjacency bitmap), uploaded once per device
     if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
     if (!g.dev[dev]) {
@@ -313,8 +372,6 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     out.launches += 2;  // init_seq_kernel + dense_kernel
     CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
     out.h2d_bytes += sizeof(hc) + recs.size();
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    out.h2d_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
 
     DenseArgs a;
     a.at4 = dg.at4;
@@ -357,41 +414,14 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
         case 16: I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st); break;
         default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
     }
-    CUDA_CHECK(cudaEventRecord(C.ev1, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    float ms = 0;
-    CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
-    out.device_ms = ms;
-
-    // readback
-    CUDA_CHECK(cudaMemcpy(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost));
-    std::vector<WStats> hs(workers);
-    CUDA_CHECK(cudaMemcpy(hs.data(), stats, workers * sizeof(WStats), cudaMemcpyDeviceToHost));
-    out.d2h_bytes += sizeof(hc) + workers * sizeof(WStats);
+    const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
     out.status = hc.status;
     out.wl_added = hc.tail;  // every enqueue ticket is one added node (root/seeds included)
     out.wl_current = (uint32_t)hc.work;
     out.wl_removed = hc.tail - out.wl_current;
     out.wl_max_size = nseeds;
+    aggregate(hs, workers, out);
     if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
-    out.worker_nodes.resize(workers);
-    out.worker_high_water.resize(workers);
-    for (uint32_t w = 0; w < workers; ++w) {
-        out.worker_nodes[w] = hs[w].nodes;
-        out.worker_high_water[w] = hs[w].high_water;
-        out.rounds += hs[w].rounds;
-        out.maxdeg += hs[w].maxdeg;
-        out.children += hs[w].children;
-        out.removals += hs[w].rm1 + hs[w].rm2 + hs[w].rmh;
-        out.rm1 += hs[w].rm1;
-        out.rm2 += hs[w].rm2;
-        out.rmh += hs[w].rmh;
-        out.dooms += hs[w].dooms;
-        out.donated += hs[w].donated;
-        out.active_cycles += hs[w].active;
-        out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
-        for (int p = 0; p < 10; ++p) out.phase[p] += hs[w].phase[p];
-    }
     if (hc.best_owner != ~0ull) {
         const uint32_t owner = (uint32_t)(hc.best_owner & 0xFFFFFFFFu);
         out.found = true;
@@ -434,7 +464,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     out.degree_bytes = 2;
     out.n_padded = npad;
 
-    auto th0 = std::chrono::steady_clock::now();
+    CUDA_CHECK(cudaEventRecord(C.evh, st));
     if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
     if (!g.dev[dev] || !g.dev[dev]->off) {
         auto dg = g.dev[dev] ? g.dev[dev] : std::make_shared<DeviceGraph>();
@@ -522,8 +552,6 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
     out.h2d_bytes += sizeof(hc) + recs.size();
     out.launches += 2;
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    out.h2d_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
 
     SparseArgs a;
     a.off = dg.off;
@@ -564,42 +592,17 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     CUDA_CHECK(cudaEventRecord(C.ev0, st));
     sparse_kernel<false><<<workers, SP_THREADS, smem, st>>>(a);
     CUDA_CHECK(cudaGetLastError());
-    CUDA_CHECK(cudaEventRecord(C.ev1, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    float ms = 0;
-    CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
-    out.device_ms = ms;
-
-    CUDA_CHECK(cudaMemcpy(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+    const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
     if (hc.status == 3)
         throw std::runtime_error("CUDA error: search stack depth exceeded the device-memory cap (" +
                                  std::to_string(bound) + " nodes per worker)");
-    std::vector<WStats> hs(workers);
-    CUDA_CHECK(cudaMemcpy(hs.data(), stats, workers * sizeof(WStats), cudaMemcpyDeviceToHost));
-    out.d2h_bytes += sizeof(hc) + workers * sizeof(WStats);
     out.status = hc.status;
     out.wl_added = hc.tail;
     out.wl_current = (uint32_t)hc.work;
     out.wl_removed = hc.tail - out.wl_current;
     out.wl_max_size = nseeds;
+    aggregate(hs, workers, out);
     if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
-    out.worker_nodes.resize(workers);
-    out.worker_high_water.resize(workers);
-    for (uint32_t w = 0; w < workers; ++w) {
-        out.worker_nodes[w] = hs[w].nodes;
-        out.worker_high_water[w] = hs[w].high_water;
-        out.rounds += hs[w].rounds;
-        out.maxdeg += hs[w].maxdeg;
-        out.children += hs[w].children;
-        out.removals += hs[w].rm1 + hs[w].rm2 + hs[w].rmh;
-        out.rm1 += hs[w].rm1;
-        out.rm2 += hs[w].rm2;
-        out.rmh += hs[w].rmh;
-        out.dooms += hs[w].dooms;
-        out.donated += hs[w].donated;
-        out.active_cycles += hs[w].active;
-        out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
-    }
     if (hc.best_owner != ~0ull) {
         const uint32_t ow = (uint32_t)(hc.best_owner & 0xFFFFFFFFu);
         out.found = true;

@@ -159,6 +159,11 @@ struct Counters {
 
 // ------------------------------------------------------------------ one search node per warp
 
+#ifndef VCG_CHILD_UNROLL
+#define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
+#endif
+constexpr int kChildUnroll = VCG_CHILD_UNROLL;
+
 template <int W, bool INSTR>
 struct WarpNode {
     static constexpr int Q = W / 4;  // uint4 groups per bitmap row
@@ -350,7 +355,7 @@ struct WarpNode {
         }
         const uint32_t keepm = alv & ~xm;  // survivors
         // rolled pass over vertex words: the survivors' lost degree, parked in shared scratch
-#pragma unroll 1
+#pragma unroll kChildUnroll
         for (int i = 0; i < W; ++i) {
             uint32_t s = 0;
             if (__any_sync(FULL, (keepm >> i) & 1u)) {

@@ -18,7 +18,7 @@ def collect_metrics(worker_nodes, phase_cycles, active_cycles):
     over workers, so the share is the cycle-weighted mean of per-worker shares."""
     total = sum(worker_nodes)
     mean = total / len(worker_nodes) if worker_nodes else 0.0
-    ratios = [(w / mean) if mean > 0 else 1.0 for w in worker_nodes]
+    ratios = [w / mean for w in worker_nodes] if mean > 0 else [1.0] * len(worker_nodes)
     shares = {}
     if active_cycles > 0:
         tracked = 0.0

@@ -9,7 +9,8 @@ def run(label, fn):
     print(json.dumps(dict(label=label, size=r["size"], feasible=r["feasible"], status=r["status"],
           nodes=r["nodes_total"], wall_ms=round(r["wall_ms"], 2), device_ms=round(r["device_ms"], 2),
           workers=len(r["worker_nodes"]), grid=r["grid_blocks"], rounds=r["rounds"], children=r["children"],
-          mnodes_per_s=round(r["nodes_total"] / max(r["device_ms"], 1e-9) / 1e3, 2), py_s=round(dt, 3))), flush=True)
+          mnodes_per_s=round(r["nodes_total"] / max(r["device_ms"], 1e-9) / 1e3, 2), py_s=round(dt, 3),
+          greedy_ms=round(r["greedy_ms"], 3), h2d_ms=round(r["h2d_ms"], 3))), flush=True)
     return r
 
 which = sys.argv[1:] or ["c1", "c3", "c5"]
