@@ -250,13 +250,13 @@ struct WarpNode {
     __device__ __forceinline__ uint32_t count_above(uint32_t lim) const {
         return __reduce_add_sync(FULL, __popc(range_mask(lim + 1u, 0xFFFFu)));
     }
-    // Can any rule fire? (an alive vertex of degree 1 or 2, or one above the limit)
-    __device__ __forceinline__ bool any_candidate(uint32_t lim) const {
-        uint32_t m = 0;
+    // Can any rule fire? (an alive vertex of degree 1 or 2, or one in `above`)
+    __device__ __forceinline__ bool any_candidate(uint32_t above) const {
+        uint32_t m = above;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const bool two = d[i] == 2u && !((nt >> i) & 1u);
-            m |= (d[i] == 1u || two || d[i] > lim ? 1u : 0u) << i;
+            m |= (d[i] == 1u || two ? 1u : 0u) << i;
         }
         return __any_sync(FULL, (m & alv) != 0);
     }
@@ -282,7 +282,15 @@ struct WarpNode {
     __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st) {
         while (edges != 0) {
             ++st.rounds;
-            if (!any_candidate(limit_for(pvc, k, snap, cc))) break;  // the final no-change round
+            // Doom test at every round start (see pass 3): a node loaded from a record is
+            // usually decided here, before any rule runs.
+            const uint32_t lim0 = limit_for(pvc, k, snap, cc);
+            const uint32_t above = range_mask(lim0 + 1u, 0xFFFFu);
+            if (__reduce_add_sync(FULL, __popc(above)) > lim0) {
+                doom = true;
+                return;
+            }
+            if (!any_candidate(above)) break;  // the final no-change round
             bool changed = false;
 #pragma unroll 1
             for (int pass = 1; pass <= 3; ++pass) {
@@ -345,6 +353,10 @@ struct WarpNode {
     }
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
+        store_child(child_lost(xl), xcnt, rec);
+    }
+    // The child's lost degrees, parked in shared scratch (ss); returns its survivors.
+    __device__ __forceinline__ uint32_t child_lost(uint32_t xl) const {
         // X in registers on every lane; xm = this lane's vertices that X removes
         uint32_t X[W];
         uint32_t xm = 0;
@@ -369,6 +381,23 @@ struct WarpNode {
             }
             ss[i * 32 + lane] = s;
         }
+        return keepm;
+    }
+    // The child is pruned whatever happens when it is visited: its cover already reaches the
+    // bound, or more survivors exceed its high-degree limit than the limit (the doom test of
+    // reduce, applied to the child's state). `snap` is the bound the child would see at best.
+    __device__ __forceinline__ bool child_doomed(uint32_t keepm, uint32_t xcnt, int pvc,
+                                                 uint32_t k, uint32_t snap) const {
+        const uint32_t c2 = cc + xcnt;
+        if (pvc ? c2 > k : c2 >= snap) return true;
+        const uint32_t lim = limit_for(pvc, k, snap, c2);
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) m |= (d[i] - ss[i * 32 + lane] > lim ? 1u : 0u) << i;
+        return __reduce_add_sync(FULL, __popc(m & keepm)) > lim;
+    }
+    __device__ __forceinline__ void store_child(uint32_t keepm, uint32_t xcnt,
+                                                unsigned char* rec) const {
         uint32_t packed[W / 2];
         uint32_t esum = 0, changed = 0;
 #pragma unroll
@@ -694,8 +723,19 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))
         // |S| + |N(v)| stays below the bound: the deferred child is never dead on arrival.)
         const uint32_t xl = x.branch_mask(v);
         const uint32_t xcnt = __reduce_add_sync(FULL, __popc(xl));
+        const bool build = !replaying || right;
+        uint32_t keepm = 0;
+        bool dead = false;
+        if (build) {
+            keepm = x.child_lost(xl);
+            // A child pruned whatever happens is visited right here (counted, as the reference
+            // counts it when it pops it) instead of being stored, queued and reloaded.
+            dead = x.child_doomed(keepm, xcnt, a.pvc, a.k, best);
+            st.nodes += dead;
+            st.dooms += dead;
+        }
         const bool oldest = a.donate_oldest && sp > 0;
-        if (!a.seq_mode && qsize < a.threshold) {
+        if (!a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
             unsigned long long seen = 0;
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
@@ -719,13 +759,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))
                 ++st.donated;
             }
         }
-        if (!replaying || right) {
+        if (build && !dead) {
             if (!child) {
                 child = slot_at(sp);
                 ++sp;
                 if (sp > st.high_water) st.high_water = sp;
             }
-            x.write_child(xl, xcnt, child);
+            x.store_child(keepm, xcnt, child);
             ++st.children;
         }
         if (publish) {
