@@ -453,7 +453,15 @@ struct CtaNode {
     template <class Cnt>
     __device__ void reduce(uint32_t snap, Cnt& st) {
         SpShared& s = *sh;
-        if (!fresh) scan(limit_for(a->pvc, a->k, snap, s.cc), true);
+        if (!fresh) {
+            const uint32_t lim0 = limit_for(a->pvc, a->k, snap, s.cc);
+            scan(lim0, true);
+            if (s.cH > lim0) {  // the doom test of phase_high, on the loaded node
+                if (threadIdx.x == 0) s.doom = 1;
+                __syncthreads();
+                return;
+            }
+        }
         while (true) {
             if (s.edges == 0) break;
             const uint32_t lim = limit_for(a->pvc, a->k, snap, s.cc);

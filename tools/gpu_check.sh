@@ -1,0 +1,9 @@
+#!/bin/bash
+# One GPU session: parity tests, then config probes for the product library and any variants.
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+python tools/probe.py c1 c3 c5 2>&1 | tee gpurun_out/probe_main.jsonl
+for v in "$@"; do
+  echo "== variant $v"
+  VCGPU_LIB=paper_2204_10402_b200/variants/$v/libvcgpu.so python tools/probe.py c5 2>&1 | tee gpurun_out/probe_$v.jsonl
+done
