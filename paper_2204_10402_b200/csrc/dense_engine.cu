@@ -209,9 +209,10 @@ const WStats* finish_and_read(DeviceCtx& C, cudaStream_t st, const Ctl* ctl, con
                               uint32_t workers, Ctl& hc, SolveOut& out) {
     CUDA_CHECK(cudaEventRecord(C.ev1, st));
     const size_t sb = (size_t)workers * sizeof(WStats);
-    unsigned char* h = static_cast<unsigned char*>(C.host.get(256 + sb));
+    constexpr size_t kStatsAt = (sizeof(Ctl) + 255) / 256 * 256;
+    unsigned char* h = static_cast<unsigned char*>(C.host.get(kStatsAt + sb));
     CUDA_CHECK(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(h + 256, stats, sb, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(h + kStatsAt, stats, sb, cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, C.ev0, C.ev1));
@@ -220,7 +221,7 @@ const WStats* finish_and_read(DeviceCtx& C, cudaStream_t st, const Ctl* ctl, con
     out.h2d_ms = ms;
     std::memcpy(&hc, h, sizeof(Ctl));
     out.d2h_bytes += sizeof(Ctl) + sb;
-    return reinterpret_cast<const WStats*>(h + 256);
+    return reinterpret_cast<const WStats*>(h + kStatsAt);
 }
 
 // Per-worker counters → the run totals (WorkerMetrics, metrics.hpp:28-41).

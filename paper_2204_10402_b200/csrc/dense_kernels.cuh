@@ -159,6 +159,9 @@ struct Counters {
 
 // ------------------------------------------------------------------ one search node per warp
 
+// Cover count of a stacked marker standing for a child proven pruned at birth.
+constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
+
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -525,9 +528,12 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
 
 template <int W, bool INSTR>
 #ifndef VCG_MINB16
-#define VCG_MINB16 2  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#define VCG_MINB16 4  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#endif               // (C5: 2 → 128 regs, 41.2 ms; 3 → 80 regs, 36.9 ms; 4 → 64 regs, 36.2 ms)
+#ifndef VCG_MINB8
+#define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
-__global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))) dense_kernel(DenseArgs a) {
+__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB16 : 1))) dense_kernel(DenseArgs a) {
     extern __shared__ uint4 smem[];
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
@@ -665,6 +671,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))
             if (__shfl_sync(FULL, stop, 0)) break;
         }
 
+        if (x.cc == DEAD_NODE) {  // a doomed child's marker: visited (counted above), pruned
+            ++st.dooms;
+            have = false;
+            continue;
+        }
         // process_node (scheduler.cpp:125-144)
         x.reduce(a.pvc, a.k, best, st);
         if (__shfl_sync(FULL, h.y, 0)) break;
@@ -728,11 +739,15 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))
         bool dead = false;
         if (build) {
             keepm = x.child_lost(xl);
-            // A child pruned whatever happens is visited right here (counted, as the reference
-            // counts it when it pops it) instead of being stored, queued and reloaded.
+            // A child pruned whatever happens is not stored, queued and reloaded: it is counted
+            // as visited right here (the reference counts it when it pops it). The one-worker
+            // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
+            // budget) must not count it — so they stack a 16-byte marker in its place instead.
             dead = x.child_doomed(keepm, xcnt, a.pvc, a.k, best);
-            st.nodes += dead;
-            st.dooms += dead;
+            if (!a.seq_mode) {
+                st.nodes += dead;
+                st.dooms += dead;
+            }
         }
         const bool oldest = a.donate_oldest && sp > 0;
         if (!a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
@@ -759,14 +774,18 @@ __global__ void __launch_bounds__(256, (W <= 8 ? 3 : (W == 16 ? VCG_MINB16 : 1))
                 ++st.donated;
             }
         }
-        if (build && !dead) {
+        if (build && (!dead || a.seq_mode)) {
             if (!child) {
                 child = slot_at(sp);
                 ++sp;
                 if (sp > st.high_water) st.high_water = sp;
             }
-            x.store_child(keepm, xcnt, child);
-            ++st.children;
+            if (dead) {
+                if (lane == 0) *reinterpret_cast<uint2*>(child) = make_uint2(DEAD_NODE, 0u);
+            } else {
+                x.store_child(keepm, xcnt, child);
+                ++st.children;
+            }
         }
         if (publish) {
             __threadfence();
