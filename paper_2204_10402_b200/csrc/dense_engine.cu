@@ -312,7 +312,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     const uint32_t block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
     const uint32_t block = 32 * block_warps;
     // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-    const size_t smem = (size_t)W * npad * 4 + (size_t)block_warps * W * 4 * 33;
+    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + (size_t)block_warps * W * 32 * 4;
     int per_sm = 1;
     switch (W) {
         case 4: per_sm = occupancy<4>(block, smem, s.instrument); break;
@@ -644,7 +644,7 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
         g.dev[dev] = dg;
     }
     const DeviceGraph& dg = *g.dev[dev];
-    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 * 33;  // see solve_on_device
+    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + 8 * (size_t)W * 32 * 4;  // see dense_scratch_base
 
     // Levels stay on the device: per level only the flags come down and the gather list of
     // surviving children goes up; the final level is copied once.

@@ -151,11 +151,32 @@ __device__ __noinline__ void poll_mailbox(volatile uint32_t* mb, int pvc, Ctl* c
     if (mb[1]) atomicExch(&ctl->cancel, 1u);
 }
 
-struct Counters {
-    unsigned long long nodes = 0, rounds = 0, maxdeg = 0, children = 0, rm1 = 0, rm2 = 0,
-                       rmh = 0, high_water = 0, donated = 0, max_queue = 0, dooms = 0;
+template <class T>
+struct CountersT {
+    T nodes = 0, rounds = 0, maxdeg = 0, children = 0, rm1 = 0, rm2 = 0, rmh = 0, donated = 0,
+      dooms = 0;
+    T high_water = 0, max_queue = 0;  // maxima
     unsigned long long phase[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
+using Counters = CountersT<unsigned long long>;
+// The dense worker keeps 32-bit deltas (half the registers) and folds them into its WStats
+// slot at every flush (at most every 64 nodes, so no delta can overflow).
+using Counters32 = CountersT<uint32_t>;
+__device__ __forceinline__ void fold_stats(WStats* o, Counters32& st) {
+    o->nodes += st.nodes;
+    o->rounds += st.rounds;
+    o->maxdeg += st.maxdeg;
+    o->children += st.children;
+    o->rm1 += st.rm1;
+    o->rm2 += st.rm2;
+    o->rmh += st.rmh;
+    o->donated += st.donated;
+    o->dooms += st.dooms;
+}
+__device__ __forceinline__ void reset_deltas(Counters32& st) {
+    st.nodes = st.rounds = st.maxdeg = st.children = st.rm1 = st.rm2 = st.rmh = st.donated =
+        st.dooms = 0;
+}
 
 // ------------------------------------------------------------------ one search node per warp
 
@@ -167,6 +188,14 @@ constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
 #endif
 constexpr int kChildUnroll = VCG_CHILD_UNROLL;
 
+// Dynamic shared memory of the dense kernels: the adjacency bitmap ([W/4][32W] uint4 groups),
+// then 8 x W/4 uint4 (reserved), then per warp W x 32 scratch words.
+extern __shared__ uint4 dense_smem[];
+template <int W>
+__device__ __forceinline__ uint32_t dense_scratch_base(uint32_t wib) {
+    return (W / 4) * (32 * W) * 4 + 8 * W + wib * W * 32;
+}
+
 template <int W, bool INSTR>
 struct WarpNode {
     static constexpr int Q = W / 4;  // uint4 groups per bitmap row
@@ -177,15 +206,22 @@ struct WarpNode {
                                      // not to close a triangle; valid until its degree changes
     uint32_t cc, edges;              // uniform
     bool doom;                       // uniform: proven to be pruned (see reduce)
-    const uint4* sat;                // shared adjacency bitmap
-    uint4* sx;                       // per-warp shared scratch: the branch mask, W words
-    uint32_t* ss;                    // per-warp shared scratch: W x 32 partial degrees
-    uint32_t npad;
+    // Shared memory is addressed through the dynamic-smem symbol with constant strides (a
+    // pointer member costs a generic→shared conversion and an address rebuild per load).
+    static constexpr uint32_t NPAD = 32 * W;  // bitmap columns (vertex slots)
+    uint32_t ssb;                    // u32 index of this warp's W x 32 scratch words
     int lane;
+
+    __device__ __forceinline__ static const uint4& grp(uint32_t q, uint32_t v) {
+        return dense_smem[q * NPAD + v];  // row v, words 4q..4q+3
+    }
+    __device__ __forceinline__ uint32_t& scratch(int i) const {
+        return reinterpret_cast<uint32_t*>(dense_smem)[ssb + i * 32 + lane];
+    }
 
     __device__ __forceinline__ bool alive(int i) const { return (alv >> i) & 1u; }
     __device__ __forceinline__ uint32_t row_word(uint32_t u, uint32_t j) const {
-        return reinterpret_cast<const uint32_t*>(sat)[((j >> 2) * npad + u) * 4 + (j & 3)];
+        return reinterpret_cast<const uint32_t*>(dense_smem)[((j >> 2) * NPAD + u) * 4 + (j & 3)];
     }
     __device__ __forceinline__ void rebuild_aw() {
 #pragma unroll
@@ -202,7 +238,7 @@ struct WarpNode {
         uint32_t touched = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const uint4 r = sat[q * npad + u];
+            const uint4 r = grp(q, u);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const uint32_t bit = (comp(r, c) >> lane) & 1u;
@@ -375,14 +411,13 @@ struct WarpNode {
             uint32_t s = 0;
             if (__any_sync(FULL, (keepm >> i) & 1u)) {
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    if ((X[4 * q] | X[4 * q + 1] | X[4 * q + 2] | X[4 * q + 3]) == 0u) continue;
-                    const uint4 c = sat[q * npad + 32 * i + lane];
+                for (int q = 0; q < Q; ++q) {  // straight-line: Q loads at constant strides
+                    const uint4 c = grp(q, 32 * i + lane);
                     s += __popc(c.x & X[4 * q]) + __popc(c.y & X[4 * q + 1]) +
                          __popc(c.z & X[4 * q + 2]) + __popc(c.w & X[4 * q + 3]);
                 }
             }
-            ss[i * 32 + lane] = s;
+            scratch(i) = s;
         }
         return keepm;
     }
@@ -396,7 +431,7 @@ struct WarpNode {
         const uint32_t lim = limit_for(pvc, k, snap, c2);
         uint32_t m = 0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) m |= (d[i] - ss[i * 32 + lane] > lim ? 1u : 0u) << i;
+        for (int i = 0; i < W; ++i) m |= (d[i] - scratch(i) > lim ? 1u : 0u) << i;
         return __reduce_add_sync(FULL, __popc(m & keepm)) > lim;
     }
     __device__ __forceinline__ void store_child(uint32_t keepm, uint32_t xcnt,
@@ -406,7 +441,7 @@ struct WarpNode {
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const bool keep = (keepm >> i) & 1u;
-            const uint32_t lost = ss[i * 32 + lane];  // own writes: no sync needed
+            const uint32_t lost = scratch(i);  // own writes: no sync needed
             const uint32_t nd = keep ? d[i] - lost : 0xFFFFu;
             esum += keep ? nd : 0u;
             changed |= (lost != 0u ? 1u : 0u) << i;
@@ -534,27 +569,24 @@ template <int W, bool INSTR>
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
 __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB16 : 1))) dense_kernel(DenseArgs a) {
-    extern __shared__ uint4 smem[];
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint32_t worker = blockIdx.x * (blockDim.x >> 5) + wib;
 
     // Stage the read-only adjacency bitmap once per CTA (coalesced 16-byte copies).
-    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) smem[t] = a.at4[t];
+    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) dense_smem[t] = a.at4[t];
     __syncthreads();
     if (worker >= a.workers) return;
 
     const unsigned long long t_start = globaltimer();
     const long long c_start = clock64();
     WarpNode<W, INSTR> x;
-    x.sat = smem;
-    x.sx = smem + Q * a.npad + wib * Q;
-    x.ss = reinterpret_cast<uint32_t*>(smem + Q * a.npad + (blockDim.x >> 5) * Q) + wib * W * 32;
-    x.npad = a.npad;
+    x.ssb = dense_scratch_base<W>(wib);
     x.lane = lane;
-    Counters st;
+    Counters32 st;
     Ctl* ctl = a.ctl;
+    WStats* const my_stats = a.stats + worker;
     unsigned char* const my_stack =
         a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes;
     // The local stack is a ring [base, base + sp) so its oldest entry can be donated.
@@ -568,7 +600,6 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     unsigned long long subtree = 0;  // StackOnly: current sub-tree id
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
-    unsigned long long nodes_flushed = 0;
 
 #pragma unroll 1
     while (true) {
@@ -654,11 +685,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
 
         // visit_and_check_limits (scheduler.cpp:63-74), batched per flush_every visits
         ++st.nodes;
-        if (st.nodes - nodes_flushed >= a.flush_every) {
+        if (st.nodes >= a.flush_every) {
             int stop = 0;
             if (lane == 0) {
                 const unsigned long long tot =
-                    atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed) + (st.nodes - nodes_flushed);
+                    atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes) + st.nodes;
                 if (a.node_budget && tot > a.node_budget) stop = 2;
                 else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) stop = 1;
                 if (stop) {
@@ -666,8 +697,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                     atomicExch(&ctl->cancel, 1u);
                 }
                 if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+                fold_stats(my_stats, st);
             }
-            nodes_flushed = st.nodes;
+            reset_deltas(st);
             if (__shfl_sync(FULL, stop, 0)) break;
         }
 
@@ -758,7 +790,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 pos = __shfl_sync(FULL, pos, 0);
                 publish = a.seq + (pos & a.ring_mask);
                 if (lane == 0) {
-                    st.max_queue = max(st.max_queue, seen);
+                    st.max_queue = max(st.max_queue, (uint32_t)seen);
                     // the slot is free once the previous lap's reader released it
                     while (ld_acquire_u64(publish) != pos) __nanosleep(32);
                 }
@@ -803,23 +835,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     }
 
     if (lane == 0) {
-        if (st.nodes > nodes_flushed) atomicAdd(&ctl->nodes_total, st.nodes - nodes_flushed);
-        WStats o;
-        o.nodes = st.nodes;
-        o.rounds = st.rounds;
-        o.maxdeg = st.maxdeg;
-        o.children = st.children;
-        o.rm1 = st.rm1;
-        o.rm2 = st.rm2;
-        o.rmh = st.rmh;
-        o.dooms = st.dooms;
-        o.high_water = st.high_water;
-        o.donated = st.donated;
-        o.active = clock64() - c_start;
-        o.max_queue = st.max_queue;
+        if (st.nodes) atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes);
+        fold_stats(my_stats, st);
+        my_stats->high_water = st.high_water;
+        my_stats->active = clock64() - c_start;
+        my_stats->max_queue = st.max_queue;
 #pragma unroll
-        for (int p = 0; p < 10; ++p) o.phase[p] = INSTR ? st.phase[p] : 0ull;
-        a.stats[worker] = o;
+        for (int p = 0; p < 10; ++p) my_stats->phase[p] = INSTR ? st.phase[p] : 0ull;
     }
 }
 
@@ -844,18 +866,13 @@ struct ExpandArgs {
 
 template <int W>
 __global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
-    extern __shared__ uint4 smem[];
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
-    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) smem[t] = a.at4[t];
+    for (uint32_t t = threadIdx.x; t < Q * a.npad; t += blockDim.x) dense_smem[t] = a.at4[t];
     __syncthreads();
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     WarpNode<W, false> x;
-    x.sat = smem;
-    x.sx = smem + Q * a.npad + (threadIdx.x >> 5) * Q;
-    x.ss = reinterpret_cast<uint32_t*>(smem + Q * a.npad + (blockDim.x >> 5) * Q) +
-           (threadIdx.x >> 5) * W * 32;
-    x.npad = a.npad;
+    x.ssb = dense_scratch_base<W>(threadIdx.x >> 5);
     x.lane = lane;
     Counters st;
 #pragma unroll 1
