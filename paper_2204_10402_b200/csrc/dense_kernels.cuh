@@ -392,10 +392,20 @@ struct WarpNode {
     }
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
-        store_child(child_lost(xl), xcnt, rec);
+        uint32_t keepm;
+        (void)child_pass<false>(xl, xcnt, 0, 0, 0, keepm);
+        store_child(keepm, xcnt, rec);
     }
-    // The child's lost degrees, parked in shared scratch (ss); returns its survivors.
-    __device__ __forceinline__ uint32_t child_lost(uint32_t xl) const {
+    // The popcount pass of the remove-N(v) child: for every survivor w, the degree it loses,
+    // |N(w) ∩ X|, parked in shared scratch; keepm = this lane's survivors.
+    // With TEST, the pass also decides whether the child is pruned whatever happens when it is
+    // visited — its cover already reaches the bound, or more survivors than its high-degree
+    // limit stay above that limit (the doom test of reduce on the child's state; `snap` is the
+    // bound it would see at best) — and stops as soon as the count passes the limit. Returns
+    // true for such a dead child (scratch is then incomplete).
+    template <bool TEST>
+    __device__ __forceinline__ bool child_pass(uint32_t xl, uint32_t xcnt, int pvc, uint32_t k,
+                                               uint32_t snap, uint32_t& keep_out) const {
         // X in registers on every lane; xm = this lane's vertices that X removes
         uint32_t X[W];
         uint32_t xm = 0;
@@ -405,7 +415,20 @@ struct WarpNode {
             xm |= ((X[j] >> lane) & 1u) << j;
         }
         const uint32_t keepm = alv & ~xm;  // survivors
-        // rolled pass over vertex words: the survivors' lost degree, parked in shared scratch
+        keep_out = keepm;
+        uint32_t lim = 0;
+        if (TEST) {
+            const uint32_t c2 = cc + xcnt;
+            if (pvc ? c2 > k : c2 >= snap) return true;
+            lim = limit_for(pvc, k, snap, c2);
+            // headroom d - lim of the survivors above the child's limit (0: not a candidate);
+            // such a survivor stays above iff it loses less than its headroom
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                scratch(i) = ((keepm >> i) & 1u) && d[i] > lim ? d[i] - lim : 0u;
+        }
+        uint32_t above = 0;
+        // rolled pass over vertex words
 #pragma unroll kChildUnroll
         for (int i = 0; i < W; ++i) {
             uint32_t s = 0;
@@ -417,22 +440,13 @@ struct WarpNode {
                          __popc(c.z & X[4 * q + 2]) + __popc(c.w & X[4 * q + 3]);
                 }
             }
+            if (TEST) {
+                above += __reduce_add_sync(FULL, s < scratch(i) ? 1u : 0u);
+                if (above > lim) return true;
+            }
             scratch(i) = s;
         }
-        return keepm;
-    }
-    // The child is pruned whatever happens when it is visited: its cover already reaches the
-    // bound, or more survivors exceed its high-degree limit than the limit (the doom test of
-    // reduce, applied to the child's state). `snap` is the bound the child would see at best.
-    __device__ __forceinline__ bool child_doomed(uint32_t keepm, uint32_t xcnt, int pvc,
-                                                 uint32_t k, uint32_t snap) const {
-        const uint32_t c2 = cc + xcnt;
-        if (pvc ? c2 > k : c2 >= snap) return true;
-        const uint32_t lim = limit_for(pvc, k, snap, c2);
-        uint32_t m = 0;
-#pragma unroll
-        for (int i = 0; i < W; ++i) m |= (d[i] - scratch(i) > lim ? 1u : 0u) << i;
-        return __reduce_add_sync(FULL, __popc(m & keepm)) > lim;
+        return false;
     }
     __device__ __forceinline__ void store_child(uint32_t keepm, uint32_t xcnt,
                                                 unsigned char* rec) const {
@@ -770,12 +784,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         uint32_t keepm = 0;
         bool dead = false;
         if (build) {
-            keepm = x.child_lost(xl);
             // A child pruned whatever happens is not stored, queued and reloaded: it is counted
             // as visited right here (the reference counts it when it pops it). The one-worker
             // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
             // budget) must not count it — so they stack a 16-byte marker in its place instead.
-            dead = x.child_doomed(keepm, xcnt, a.pvc, a.k, best);
+            dead = x.template child_pass<true>(xl, xcnt, a.pvc, a.k, best, keepm);
             if (!a.seq_mode) {
                 st.nodes += dead;
                 st.dooms += dead;
