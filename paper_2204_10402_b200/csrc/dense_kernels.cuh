@@ -235,18 +235,14 @@ struct WarpNode {
     __device__ __forceinline__ void remove_vertex(uint32_t u) {
         uint32_t du = lane < W ? __popc(row_word(u, lane) & aw) : 0u;
         du = __reduce_add_sync(FULL, du);
-        uint32_t touched = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint4 r = grp(q, u);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t bit = (comp(r, c) >> lane) & 1u;
-                d[4 * q + c] -= bit;
-                touched |= bit << (4 * q + c);
-            }
+            for (int c = 0; c < 4; ++c) d[4 * q + c] -= (comp(r, c) >> lane) & 1u;
         }
-        nt &= ~touched;  // a changed degree invalidates the cached non-triangle verdict
+        // (no verdict to invalidate: a cached non-triangle verdict is consulted only at degree
+        // two, and a degree never rises, so once it leaves two the stale bit is never read)
         if (lane == (int)(u & 31)) alv &= ~(1u << (u >> 5));
         if (lane == (int)(u >> 5)) aw &= ~(1u << (u & 31));
         cc += 1;
@@ -451,21 +447,20 @@ struct WarpNode {
     __device__ __forceinline__ void store_child(uint32_t keepm, uint32_t xcnt,
                                                 unsigned char* rec) const {
         uint32_t packed[W / 2];
-        uint32_t esum = 0, changed = 0;
+        uint32_t esum = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const bool keep = (keepm >> i) & 1u;
             const uint32_t lost = scratch(i);  // own writes: no sync needed
             const uint32_t nd = keep ? d[i] - lost : 0xFFFFu;
             esum += keep ? nd : 0u;
-            changed |= (lost != 0u ? 1u : 0u) << i;
             if (i & 1) packed[i / 2] |= nd << 16;
             else packed[i / 2] = nd;
         }
         const uint32_t e2 = __reduce_add_sync(FULL, esum);
         if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc + xcnt, e2 / 2);
         store_degrees(rec, packed);
-        store_nt(rec, nt & keepm & ~changed);  // verdicts of survivors whose degree held
+        store_nt(rec, nt & keepm);  // stale bits of vertices below degree two are never read
     }
     // The cached non-triangle verdicts travel with the record (one word per lane).
     __device__ __forceinline__ void store_nt(unsigned char* rec, uint32_t m) const {
