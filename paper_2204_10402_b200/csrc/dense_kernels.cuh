@@ -572,8 +572,8 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
 
 template <int W, bool INSTR>
 #ifndef VCG_MINB16
-#define VCG_MINB16 4  // CTAs of 8 warps per SM targeted by the W=16 register allocation
-#endif               // (C5: 2 → 128 regs, 41.2 ms; 3 → 80 regs, 36.9 ms; 4 → 64 regs, 36.2 ms)
+#define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#endif               // (C5 now: 3 → 80 regs, 26.6 ms; 4 → 64 regs + spills, 28.0 ms)
 #ifndef VCG_MINB8
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
