@@ -252,17 +252,24 @@ struct WarpNode {
     // the reference's ascending pass would act on. -1 if none.
     // Bit-sliced: each lane builds the mask of its own candidates (bit i = vertex 32*i + lane),
     // and one REDUX picks the smallest id — no per-word ballots, no branches.
-    __device__ __forceinline__ uint32_t range_mask(uint32_t lo, uint32_t hi) const {
-        const uint32_t span = hi - lo;
+    __device__ __forceinline__ uint32_t eq_mask(uint32_t c) const {
         uint32_t m = 0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) m |= (d[i] - lo <= span ? 1u : 0u) << i;
+        for (int i = 0; i < W; ++i) m |= (d[i] == c ? 1u : 0u) << i;
         return m & alv;
     }
-    __device__ __forceinline__ int find_first(int pos, uint32_t lo, uint32_t hi,
-                                              uint32_t skip) const {
+    // Alive vertices of degree > lim: the sign of lim - d (both < 2^16) funnel-shifted into the
+    // mask, two instructions per word.
+    __device__ __forceinline__ uint32_t above_mask(uint32_t lim) const {
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = W - 1; i >= 0; --i) m = __funnelshift_l(lim - d[i], m, 1);
+        return m & alv;
+    }
+    // pass 1, 2: degree == c; pass 3: degree > c
+    __device__ __forceinline__ int find_first(int pos, int pass, uint32_t c, uint32_t skip) const {
         const uint32_t pi = (uint32_t)pos >> 5;
-        uint32_t m = range_mask(lo, hi) & ~skip;
+        uint32_t m = (pass == 3 ? above_mask(c) : eq_mask(c)) & ~skip;
         m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
         const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
         const uint32_t v = __reduce_min_sync(FULL, key);
@@ -283,7 +290,7 @@ struct WarpNode {
     }
     // Number of alive vertices of degree > lim (degree > lim >= 0 implies degree > 0).
     __device__ __forceinline__ uint32_t count_above(uint32_t lim) const {
-        return __reduce_add_sync(FULL, __popc(range_mask(lim + 1u, 0xFFFFu)));
+        return __reduce_add_sync(FULL, __popc(above_mask(lim)));
     }
     // Can any rule fire? (an alive vertex of degree 1 or 2, or one in `above`)
     __device__ __forceinline__ bool any_candidate(uint32_t above) const {
@@ -320,7 +327,7 @@ struct WarpNode {
             // Doom test at every round start (see pass 3): a node loaded from a record is
             // usually decided here, before any rule runs.
             const uint32_t lim0 = limit_for(pvc, k, snap, cc);
-            const uint32_t above = range_mask(lim0 + 1u, 0xFFFFu);
+            const uint32_t above = above_mask(lim0);
             if (__reduce_add_sync(FULL, __popc(above)) > lim0) {
                 doom = true;
                 return;
@@ -330,22 +337,21 @@ struct WarpNode {
 #pragma unroll 1
             for (int pass = 1; pass <= 3; ++pass) {
                 long long t0 = INSTR ? clock64() : 0;
-                uint32_t lo = pass, hi = pass;
+                uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
                 if (pass == 3) {
                     const uint32_t lim = limit_for(pvc, k, snap, cc);
                     // Every alive vertex above the limit at pass start is removed by this pass
                     // (each removal lowers the limit by one and any degree by at most one), so
                     // more than `lim` of them take |S| past the bound: the node is pruned.
                     if (count_above(lim) > lim) doom = true;
-                    lo = lim + 1u;
-                    hi = 0xFFFFu;
+                    c = lim;
                 }
                 int pos = 0;
 #pragma unroll 1
                 while (!doomed(pvc, k, snap)) {
                     // (a degree-two vertex already known not to close a triangle is skipped:
                     // its partners are unchanged while its degree is, so the test would fail)
-                    const int v = find_first(pos, lo, hi, pass == 2 ? nt : 0u);
+                    const int v = find_first(pos, pass, c, pass == 2 ? nt : 0u);
                     if (v < 0) break;
                     pos = v + 1;
                     int u0 = v, u1 = -1;
@@ -370,7 +376,7 @@ struct WarpNode {
                         st.rm2 += pass == 2;
                         st.rmh += pass == 3;
                     }
-                    if (pass == 3) lo = limit_for(pvc, k, snap, cc) + 1u;  // :50-56
+                    if (pass == 3) c = limit_for(pvc, k, snap, cc);  // :50-56
                 }
                 if (INSTR) st.phase[PH_DEG1 + pass - 1] += clock64() - t0;
                 if (doomed(pvc, k, snap)) return;
@@ -421,7 +427,7 @@ struct WarpNode {
             // such a survivor stays above iff it loses less than its headroom
 #pragma unroll
             for (int i = 0; i < W; ++i)
-                scratch(i) = ((keepm >> i) & 1u) && d[i] > lim ? d[i] - lim : 0u;
+                scratch(i) = ((keepm >> i) & 1u) ? (uint32_t)max((int)(d[i] - lim), 0) : 0u;
         }
         uint32_t above = 0;
         // rolled pass over vertex words
