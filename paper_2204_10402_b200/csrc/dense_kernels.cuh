@@ -183,6 +183,13 @@ __device__ __forceinline__ void reset_deltas(Counters32& st) {
 // Cover count of a stacked marker standing for a child proven pruned at birth.
 constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
 
+#ifndef VCG_POLL_EVERY
+#define VCG_POLL_EVERY 8  // nodes between reads of the control line (power of two)
+#endif
+constexpr uint32_t kPoll = VCG_POLL_EVERY;
+#ifndef VCG_PASS_SKIP
+#define VCG_PASS_SKIP 1  // round-start candidate masks: skip empty passes, reuse the first scan
+#endif
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -268,8 +275,11 @@ struct WarpNode {
     }
     // pass 1, 2: degree == c; pass 3: degree > c
     __device__ __forceinline__ int find_first(int pos, int pass, uint32_t c, uint32_t skip) const {
+        return first_in((pass == 3 ? above_mask(c) : eq_mask(c)) & ~skip, pos);
+    }
+    // smallest vertex id >= pos in the bit-sliced candidate mask m (bit i = vertex 32*i + lane)
+    __device__ __forceinline__ int first_in(uint32_t m, int pos) const {
         const uint32_t pi = (uint32_t)pos >> 5;
-        uint32_t m = (pass == 3 ? above_mask(c) : eq_mask(c)) & ~skip;
         m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
         const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
         const uint32_t v = __reduce_min_sync(FULL, key);
@@ -332,26 +342,65 @@ struct WarpNode {
                 doom = true;
                 return;
             }
+#if VCG_PASS_SKIP
+            // Candidate masks of the three passes at round start; they stay exact until the next
+            // removal, so a pass without candidates is skipped and the first scan of a pass
+            // reuses its mask.
+            uint32_t m1 = 0, m2 = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                m1 |= (d[i] == 1u ? 1u : 0u) << i;
+                m2 |= (d[i] == 2u ? 1u : 0u) << i;
+            }
+            m1 &= alv;
+            m2 &= alv & ~nt;
+            if (!__any_sync(FULL, (m1 | m2 | above) != 0)) break;  // the final no-change round
+            bool removed = false;  // a removal happened since the round-start masks
+#else
             if (!any_candidate(above)) break;  // the final no-change round
+#endif
             bool changed = false;
 #pragma unroll 1
             for (int pass = 1; pass <= 3; ++pass) {
                 long long t0 = INSTR ? clock64() : 0;
                 uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
+#if VCG_PASS_SKIP
+                uint32_t cand = pass == 1 ? m1 : pass == 2 ? m2 : above;
+                bool stale = removed;  // cand must be recomputed before use
+#endif
                 if (pass == 3) {
                     const uint32_t lim = limit_for(pvc, k, snap, cc);
                     // Every alive vertex above the limit at pass start is removed by this pass
                     // (each removal lowers the limit by one and any degree by at most one), so
                     // more than `lim` of them take |S| past the bound: the node is pruned.
+#if VCG_PASS_SKIP
+                    if (removed) {  // (otherwise lim == lim0 and the round-start test holds)
+                        cand = above_mask(lim);
+                        if (__reduce_add_sync(FULL, __popc(cand)) > lim) doom = true;
+                        stale = false;
+                    }
+#else
                     if (count_above(lim) > lim) doom = true;
+#endif
                     c = lim;
                 }
+#if VCG_PASS_SKIP
+                if (!stale && !__any_sync(FULL, cand != 0)) continue;
+#endif
                 int pos = 0;
 #pragma unroll 1
                 while (!doomed(pvc, k, snap)) {
                     // (a degree-two vertex already known not to close a triangle is skipped:
                     // its partners are unchanged while its degree is, so the test would fail)
+#if VCG_PASS_SKIP
+                    if (stale) {
+                        cand = (pass == 3 ? above_mask(c) : eq_mask(c)) & ~(pass == 2 ? nt : 0u);
+                        stale = false;
+                    }
+                    const int v = first_in(cand, pos);
+#else
                     const int v = find_first(pos, pass, c, pass == 2 ? nt : 0u);
+#endif
                     if (v < 0) break;
                     pos = v + 1;
                     int u0 = v, u1 = -1;
@@ -372,6 +421,9 @@ struct WarpNode {
                         if (u < 0) break;
                         remove_vertex((uint32_t)u);
                         changed = true;
+#if VCG_PASS_SKIP
+                        removed = stale = true;
+#endif
                         st.rm1 += pass == 1;
                         st.rm2 += pass == 2;
                         st.rmh += pass == 3;
@@ -615,6 +667,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     unsigned long long subtree = 0;  // StackOnly: current sub-tree id
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
+    uint32_t qsize = 0, polls = kPoll - 1;  // (the first node polls)
 
 #pragma unroll 1
     while (true) {
@@ -677,7 +730,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             }
             x.load(src);
             if (release) {
-                __threadfence();
+                // every lane's read of the slot is ordered before lane 0's release by the
+                // warp barrier (cumulativity): no full fence needed
                 __syncwarp();
                 if (lane == 0) {
                     st_release_u64(release, pos + a.ring_mask + 1);  // free for the next lap
@@ -691,9 +745,14 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         // Issue the read of the hot control line now, consume it after the reduction (its L2
         // latency hides behind the rule passes). The rules use the bound seen at the previous
         // node (a stale, larger bound only prunes less).
+        // Every worker polling the one control line at every node queues thousands of reads on
+        // one L2 slice (and the scoreboard wait lands inside the reduction), so it is polled
+        // every kPoll nodes; in between the warp uses the last bound / queue size it saw (a
+        // stale bound only prunes less; the queue size only steers donation).
+        const bool poll = (++polls & (kPoll - 1)) == 0;
         uint4 h = make_uint4(0, 0, 0, 0);
         unsigned long long hw = 0;
-        if (lane == 0) {
+        if (poll && lane == 0) {
             h = ld_volatile_v4(ctl);
             hw = ld_relaxed_u64(&ctl->work);
         }
@@ -725,9 +784,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         }
         // process_node (scheduler.cpp:125-144)
         x.reduce(a.pvc, a.k, best, st);
-        if (__shfl_sync(FULL, h.y, 0)) break;
-        if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
-        const uint32_t qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+        if (poll) {
+            if (__shfl_sync(FULL, h.y, 0)) break;
+            if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
+            qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+        }
         const bool prune = x.doom || should_prune(a.pvc, a.k, best, x.cc, x.edges);
         st.dooms += x.doom;
         if (prune) {
@@ -834,8 +895,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             }
         }
         if (publish) {
-            __threadfence();
-            __syncwarp();
+            __syncwarp();  // (the release by lane 0 is cumulative over the warp's stores)
             if (lane == 0) st_release_u64(publish, pos + 1);
         }
         if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
