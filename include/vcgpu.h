@@ -104,7 +104,9 @@ typedef struct {
                                    VCG_RULES_PARALLEL (block-parallel rule rounds) */
     uint32_t block_warps;       /* warps per CTA, 0 = auto */
     int32_t engine;             /* 0 auto, 1 dense (n <= 1024, warp per node),
-                                   2 sparse (any n, CTA per node) */
+                                   2 sparse (any n, CTA per node),
+                                   3 dense without compact renumbering (every node in the wide
+                                     32*W-slot layout; for A/B tests) */
     int32_t instrument;         /* 1: per-worker phase cycle counters */
     int32_t donate_oldest;      /* 1: when donating, hand over the OLDEST stacked node (largest
                                    expected sub-tree) and stack the new child; 0: donate the new

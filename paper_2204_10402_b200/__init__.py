@@ -190,7 +190,7 @@ def load_graph(path, fmt=None, complement_input=False) -> BaseGraph:
 _STRATEGIES = {"hybrid": _n.VCG_HYBRID, "gpu": _n.VCG_HYBRID, "seq": _n.VCG_SEQ,
                "stackonly": _n.VCG_STACKONLY}
 _RULES = {"reference": 0, "parallel": 1}
-_ENGINES = {"auto": 0, "dense": 1, "sparse": 2}
+_ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3}
 
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,

@@ -166,9 +166,12 @@ std::vector<uint32_t> build_bitmap(const Graph& g, uint32_t W, uint32_t npad) {
     return at;
 }
 
-// Node record: [cc, edges, 0, 0] + lane-major u16 degrees (2W bytes per lane) + one word per
-// lane of cached degree-two non-triangle verdicts.
-size_t dense_record_bytes(uint32_t W) { return 16 + 64 * (size_t)W + 128; }
+// Node record: the larger of the wide layout ([cc, edges, kind, 0] + lane-major u16 degrees
+// (2W bytes per lane) + one word per lane of cached degree-two non-triangle verdicts) and the
+// compact layout (CompactNode).
+size_t dense_record_bytes(uint32_t W) {
+    return std::max<size_t>(16 + 64 * (size_t)W + 128, kCompactRecordBytes);
+}
 
 // Pack one node record.
 void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint32_t* deg,
@@ -403,6 +406,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
     a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
     a.donate_oldest = s.donate_oldest ? 1 : 0;
+    a.compact = s.engine == 3 ? 0 : 1;
     a.stackonly = s.strategy == 2 ? 1 : 0;
     a.depth = s.depth;
     a.mailbox = s.mailbox;

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace vcg {
 
@@ -87,6 +88,7 @@ struct DenseArgs {
     uint32_t backoff_ns;
     int seq_mode;             // never donate (solve_*_seq semantics)
     int donate_oldest;        // donate the bottom (oldest) stacked node instead of the new child
+    int compact;              // renumber nodes with <= 64 alive vertices (CompactNode)
     int stackonly;            // StackOnly strategy (scheduler.cpp:214-297): claim sub-tree ids
     uint32_t depth;           // StackOnly sub-tree depth (2^depth sub-trees)
     volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out,
@@ -182,14 +184,13 @@ __device__ __forceinline__ void reset_deltas(Counters32& st) {
 
 // Cover count of a stacked marker standing for a child proven pruned at birth.
 constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
+// Record kinds (header word 2): wide (WarpNode layout) or compact (CompactNode layout).
+constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1;
 
 #ifndef VCG_POLL_EVERY
 #define VCG_POLL_EVERY 8  // nodes between reads of the control line (power of two)
 #endif
 constexpr uint32_t kPoll = VCG_POLL_EVERY;
-#ifndef VCG_PASS_SKIP
-#define VCG_PASS_SKIP 1  // round-start candidate masks: skip empty passes, reuse the first scan
-#endif
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -205,6 +206,7 @@ __device__ __forceinline__ uint32_t dense_scratch_base(uint32_t wib) {
 
 template <int W, bool INSTR>
 struct WarpNode {
+    static constexpr bool kInstr = INSTR;
     static constexpr int Q = W / 4;  // uint4 groups per bitmap row
     uint32_t d[W];                   // degree of vertex 32*i + lane (meaningless once removed)
     uint32_t alv;                    // bit i: vertex 32*i + lane is alive (not in the cover)
@@ -327,114 +329,30 @@ struct WarpNode {
         return doom || (pvc ? cc > k : cc >= snap);
     }
 
-    // reduce_loop (reductions.cpp:63-90): rounds of {degree-one, degree-two-triangle,
-    // high-degree} passes, each an ascending scan acting at visit time, until a round changes
-    // nothing. One rolled pass loop; the pass selects the candidate range [lo, hi].
+    // reduce_loop (reductions.cpp:63-90), shared with the compact node (reduce_node below)
     template <class Cnt>
-    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st) {
-        while (edges != 0) {
-            ++st.rounds;
-            // Doom test at every round start (see pass 3): a node loaded from a record is
-            // usually decided here, before any rule runs.
-            const uint32_t lim0 = limit_for(pvc, k, snap, cc);
-            const uint32_t above = above_mask(lim0);
-            if (__reduce_add_sync(FULL, __popc(above)) > lim0) {
-                doom = true;
-                return;
-            }
-#if VCG_PASS_SKIP
-            // Candidate masks of the three passes at round start; they stay exact until the next
-            // removal, so a pass without candidates is skipped and the first scan of a pass
-            // reuses its mask.
-            uint32_t m1 = 0, m2 = 0;
+    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st);
+    // candidate masks of passes 1 and 2 (alive, degree one / degree two without a cached
+    // non-triangle verdict)
+    __device__ __forceinline__ void deg_masks(uint32_t& m1, uint32_t& m2) const {
+        m1 = m2 = 0;
 #pragma unroll
-            for (int i = 0; i < W; ++i) {
-                m1 |= (d[i] == 1u ? 1u : 0u) << i;
-                m2 |= (d[i] == 2u ? 1u : 0u) << i;
-            }
-            m1 &= alv;
-            m2 &= alv & ~nt;
-            if (!__any_sync(FULL, (m1 | m2 | above) != 0)) break;  // the final no-change round
-            bool removed = false;  // a removal happened since the round-start masks
-#else
-            if (!any_candidate(above)) break;  // the final no-change round
-#endif
-            bool changed = false;
-#pragma unroll 1
-            for (int pass = 1; pass <= 3; ++pass) {
-                long long t0 = INSTR ? clock64() : 0;
-                uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
-#if VCG_PASS_SKIP
-                uint32_t cand = pass == 1 ? m1 : pass == 2 ? m2 : above;
-                bool stale = removed;  // cand must be recomputed before use
-#endif
-                if (pass == 3) {
-                    const uint32_t lim = limit_for(pvc, k, snap, cc);
-                    // Every alive vertex above the limit at pass start is removed by this pass
-                    // (each removal lowers the limit by one and any degree by at most one), so
-                    // more than `lim` of them take |S| past the bound: the node is pruned.
-#if VCG_PASS_SKIP
-                    if (removed) {  // (otherwise lim == lim0 and the round-start test holds)
-                        cand = above_mask(lim);
-                        if (__reduce_add_sync(FULL, __popc(cand)) > lim) doom = true;
-                        stale = false;
-                    }
-#else
-                    if (count_above(lim) > lim) doom = true;
-#endif
-                    c = lim;
-                }
-#if VCG_PASS_SKIP
-                if (!stale && !__any_sync(FULL, cand != 0)) continue;
-#endif
-                int pos = 0;
-#pragma unroll 1
-                while (!doomed(pvc, k, snap)) {
-                    // (a degree-two vertex already known not to close a triangle is skipped:
-                    // its partners are unchanged while its degree is, so the test would fail)
-#if VCG_PASS_SKIP
-                    if (stale) {
-                        cand = (pass == 3 ? above_mask(c) : eq_mask(c)) & ~(pass == 2 ? nt : 0u);
-                        stale = false;
-                    }
-                    const int v = first_in(cand, pos);
-#else
-                    const int v = find_first(pos, pass, c, pass == 2 ? nt : 0u);
-#endif
-                    if (v < 0) break;
-                    pos = v + 1;
-                    int u0 = v, u1 = -1;
-                    if (pass < 3) {
-                        int p0, p1;
-                        first_neighbors(v, p0, p1);
-                        u0 = p0;  // degree one: its unique alive neighbour (reductions.cpp:7-19)
-                        if (pass == 2) {  // degree two: both partners iff adjacent (:22-40)
-                            const bool tri = (row_word(p0, p1 >> 5) >> (p1 & 31)) & 1u;
-                            u0 = tri ? p0 : -1;
-                            u1 = tri ? p1 : -1;
-                            if (!tri && lane == (v & 31)) nt |= 1u << (v >> 5);
-                        }
-                    }
-#pragma unroll 1
-                    for (int t = 0; t < 2; ++t) {
-                        const int u = t ? u1 : u0;
-                        if (u < 0) break;
-                        remove_vertex((uint32_t)u);
-                        changed = true;
-#if VCG_PASS_SKIP
-                        removed = stale = true;
-#endif
-                        st.rm1 += pass == 1;
-                        st.rm2 += pass == 2;
-                        st.rmh += pass == 3;
-                    }
-                    if (pass == 3) c = limit_for(pvc, k, snap, cc);  // :50-56
-                }
-                if (INSTR) st.phase[PH_DEG1 + pass - 1] += clock64() - t0;
-                if (doomed(pvc, k, snap)) return;
-            }
-            if (!changed) break;
+        for (int i = 0; i < W; ++i) {
+            m1 |= (d[i] == 1u ? 1u : 0u) << i;
+            m2 |= (d[i] == 2u ? 1u : 0u) << i;
         }
+        m1 &= alv;
+        m2 &= alv & ~nt;
+    }
+    __device__ __forceinline__ bool is_edge(uint32_t p, uint32_t q) const {
+        return (row_word(p, q >> 5) >> (q & 31)) & 1u;
+    }
+    __device__ __forceinline__ void mark_nt(uint32_t v) {
+        if (lane == (int)(v & 31)) nt |= 1u << (v >> 5);
+    }
+    // alive vertices (warp-uniform)
+    __device__ __forceinline__ uint32_t alive_count() const {
+        return __reduce_add_sync(FULL, __popc(alv));
     }
 
     // The remove-N(v) child (search_node.cpp:27-32 on a clone) written straight to a record:
@@ -443,6 +361,25 @@ struct WarpNode {
     // Lane j < W: word j of X = N(v) ∩ alive (the vertices the remove-N(v) child covers).
     __device__ __forceinline__ uint32_t branch_mask(uint32_t v) const {
         return lane < W ? (row_word(v, lane) & aw) : 0u;
+    }
+    // The child interface shared with CompactNode (see the kernel's branch step).
+    struct Child {
+        uint32_t xl, xcnt, keepm;
+    };
+    __device__ __forceinline__ void child_begin(uint32_t v, Child& c) const {
+        c.xl = branch_mask(v);
+        c.xcnt = __reduce_add_sync(FULL, __popc(c.xl));
+    }
+    template <bool TEST>
+    __device__ __forceinline__ bool child_pass(Child& c, int pvc, uint32_t k, uint32_t snap) const {
+        return child_pass<TEST>(c.xl, c.xcnt, pvc, k, snap, c.keepm);
+    }
+    __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
+        store_child(c.keepm, c.xcnt, rec);
+    }
+    template <int WW>
+    __device__ __forceinline__ uint32_t cover_word(uint32_t*) const {
+        return cover_word();
     }
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
@@ -516,7 +453,7 @@ struct WarpNode {
             else packed[i / 2] = nd;
         }
         const uint32_t e2 = __reduce_add_sync(FULL, esum);
-        if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc + xcnt, e2 / 2);
+        if (lane == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(cc + xcnt, e2 / 2, REC_WIDE, 0u);
         store_degrees(rec, packed);
         store_nt(rec, nt & keepm);  // stale bits of vertices below degree two are never read
     }
@@ -543,23 +480,9 @@ struct WarpNode {
             if (i & 1) packed[i / 2] |= h << 16;
             else packed[i / 2] = h;
         }
-        if (lane == 0) *reinterpret_cast<uint2*>(rec) = make_uint2(cc, edges);
+        if (lane == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(cc, edges, REC_WIDE, 0u);
         store_degrees(rec, packed);
         store_nt(rec, nt);
-    }
-    // Moves one record between stack and worklist memory without unpacking it.
-    __device__ __forceinline__ void copy_record(const unsigned char* src, unsigned char* dst) const {
-        const unsigned char* p = src + 16 + lane * (2 * W);
-        unsigned char* q = dst + 16 + lane * (2 * W);
-        if constexpr (W == 4) {
-            *reinterpret_cast<uint2*>(q) = __ldcg(reinterpret_cast<const uint2*>(p));
-        } else {
-#pragma unroll
-            for (int t = 0; t < W / 8; ++t)
-                reinterpret_cast<uint4*>(q)[t] = __ldcg(reinterpret_cast<const uint4*>(p) + t);
-        }
-        store_nt(dst, __ldcg(reinterpret_cast<const uint32_t*>(src + 16 + 64 * W) + lane));
-        if (lane == 0) *reinterpret_cast<uint4*>(dst) = __ldcg(reinterpret_cast<const uint4*>(src));
     }
     // Loads a record through L2 (it may come from another SM's worklist donation).
     __device__ __forceinline__ void load(const unsigned char* rec) {
@@ -607,6 +530,351 @@ struct WarpNode {
     }
 };
 
+// ------------------------------------------------------------------ compact search node
+
+// Deep in the tree only a few dozen vertices are still alive (C5: 34 on average at a branch, of
+// 500), yet the wide node scans all 32*W slots and reads the whole bitmap per child. Once at most
+// 64 are alive, the node is renumbered: slot c (0..63) = the c-th alive vertex in id order, at
+// lane c & 31, half c >> 5, and each lane keeps the INDUCED adjacency rows of its two slots as
+// 64-bit masks in registers. Removing a slot, finding a partner, the triangle test, the whole
+// remove-N(v) child and its doom test become a handful of shuffles and popcounts, with no shared
+// memory traffic. Renumbering keeps the id order, so every rule acts on the same vertex as in
+// the wide layout (and in the reference): node counts are unchanged. The alive set only shrinks,
+// so every descendant of a compact node stays compact with the same slots.
+constexpr uint32_t kCompactSlots = 64;
+// Compact record: {cc, edges, kind, 0, alive lo, alive hi, 0, 0} + per lane {row of slot lane,
+// row of slot lane+32} (16 B) + per lane packed ids (2 x u16) + per lane cached verdicts.
+constexpr uint32_t kCompactRecordBytes = 32 + 32 * 16 + 32 * 4 + 32 * 4;
+
+template <bool INSTR>
+struct CompactNode {
+    static constexpr bool kInstr = INSTR;
+    static constexpr int H = 2;          // slots per lane
+    unsigned long long r[H];             // induced row of slot 32*i + lane (bit c: slot c adjacent)
+    uint32_t d[H];                       // degree of slot 32*i + lane (meaningless once removed)
+    uint32_t alv;                        // bit i: slot 32*i + lane is alive
+    unsigned long long am;               // alive slots (warp-uniform)
+    uint32_t nt;                         // bit i: cached degree-two non-triangle verdict
+    uint32_t ids;                        // vertex ids of slots lane (low 16) and lane + 32 (high)
+    uint32_t cc, edges;                  // uniform
+    bool doom;                           // uniform
+    int lane;
+
+    __device__ __forceinline__ bool alive(int i) const { return (alv >> i) & 1u; }
+    // the row of slot u on every lane
+    __device__ __forceinline__ unsigned long long row(uint32_t u) const {
+        return __shfl_sync(FULL, (u >> 5) ? r[1] : r[0], u & 31);
+    }
+    __device__ __forceinline__ void remove_vertex(uint32_t u) {  // search_node.cpp:16-25
+        const unsigned long long ru = row(u);
+        const uint32_t du = __popcll(ru & am);
+#pragma unroll
+        for (int i = 0; i < H; ++i) d[i] -= (uint32_t)(ru >> (32 * i + lane)) & 1u;
+        if (lane == (int)(u & 31)) alv &= ~(1u << (u >> 5));
+        am &= ~(1ull << u);
+        cc += 1;
+        edges -= du;
+    }
+    __device__ __forceinline__ uint32_t eq_mask(uint32_t c) const {
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) m |= (d[i] == c ? 1u : 0u) << i;
+        return m & alv;
+    }
+    __device__ __forceinline__ uint32_t above_mask(uint32_t lim) const {
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = H - 1; i >= 0; --i) m = __funnelshift_l(lim - d[i], m, 1);
+        return m & alv;
+    }
+    __device__ __forceinline__ void deg_masks(uint32_t& m1, uint32_t& m2) const {
+        m1 = eq_mask(1u);
+        m2 = eq_mask(2u) & ~nt;
+    }
+    __device__ __forceinline__ int first_in(uint32_t m, int pos) const {
+        const uint32_t pi = (uint32_t)pos >> 5;
+        m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
+        const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
+        const uint32_t v = __reduce_min_sync(FULL, key);
+        return v == FULL ? -1 : (int)v;
+    }
+    __device__ __forceinline__ void first_neighbors(uint32_t v, int& p0, int& p1) const {
+        unsigned long long x = row(v) & am;
+        p0 = __ffsll((long long)x) - 1;
+        x &= x - 1;
+        p1 = x ? __ffsll((long long)x) - 1 : -1;
+    }
+    __device__ __forceinline__ bool is_edge(uint32_t p, uint32_t q) const {
+        return (row(p) >> q) & 1ull;
+    }
+    __device__ __forceinline__ void mark_nt(uint32_t v) {
+        if (lane == (int)(v & 31)) nt |= 1u << (v >> 5);
+    }
+    __device__ __forceinline__ uint32_t argmax() const {  // search_node.cpp:34-46
+        uint32_t mx = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+            mx = max(mx, alive(i) ? ((d[i] << 11) | (2047u - (32u * i + lane))) : 0u);
+        mx = __reduce_max_sync(FULL, mx);
+        return 2047u - (mx & 2047u);
+    }
+    __device__ __forceinline__ bool doomed(int pvc, uint32_t k, uint32_t snap) const {
+        return doom || (pvc ? cc > k : cc >= snap);
+    }
+    template <class Cnt>
+    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st);
+
+    // ---- the remove-N(v) child (search_node.cpp:27-32 on a clone)
+    struct Child {
+        unsigned long long X;  // slots the child covers: N(v) ∩ alive
+        uint32_t xcnt, keepm;  // |X|; this lane's surviving slots
+        uint32_t nd[H];        // the survivors' degrees in the child
+    };
+    __device__ __forceinline__ void child_begin(uint32_t v, Child& c) const {
+        c.X = row(v) & am;
+        c.xcnt = __popcll(c.X);
+    }
+    // Degrees of the child; with TEST, true if it is pruned whatever happens when visited (its
+    // cover reaches the bound, or more survivors than its limit stay above it — the round-start
+    // doom test of reduce_node on the child's state).
+    template <bool TEST>
+    __device__ __forceinline__ bool child_pass(Child& c, int pvc, uint32_t k, uint32_t snap) const {
+        uint32_t xm = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            xm |= ((uint32_t)(c.X >> (32 * i + lane)) & 1u) << i;
+            c.nd[i] = d[i] - __popcll(r[i] & c.X);
+        }
+        c.keepm = alv & ~xm;
+        if (!TEST) return false;
+        const uint32_t c2 = cc + c.xcnt;
+        if (pvc ? c2 > k : c2 >= snap) return true;
+        const uint32_t lim = limit_for(pvc, k, snap, c2);
+        uint32_t above = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) above += ((c.keepm >> i) & 1u) && c.nd[i] > lim;
+        return __reduce_add_sync(FULL, above) > lim;
+    }
+    __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
+        uint32_t esum = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) esum += ((c.keepm >> i) & 1u) ? c.nd[i] : 0u;
+        const uint32_t e2 = __reduce_add_sync(FULL, esum);
+        store(rec, cc + c.xcnt, e2 / 2, am & ~c.X, nt & c.keepm);
+    }
+    __device__ __forceinline__ void store(unsigned char* rec, uint32_t rcc, uint32_t redges,
+                                          unsigned long long ram, uint32_t rnt) const {
+        if (lane == 0) {
+            reinterpret_cast<uint4*>(rec)[0] = make_uint4(rcc, redges, REC_COMPACT, 0u);
+            reinterpret_cast<uint4*>(rec)[1] =
+                make_uint4((uint32_t)ram, (uint32_t)(ram >> 32), 0u, 0u);
+        }
+        reinterpret_cast<uint4*>(rec + 32)[lane] =
+            make_uint4((uint32_t)r[0], (uint32_t)(r[0] >> 32), (uint32_t)r[1], (uint32_t)(r[1] >> 32));
+        reinterpret_cast<uint32_t*>(rec + 32 + 512)[lane] = ids;
+        reinterpret_cast<uint32_t*>(rec + 32 + 512 + 128)[lane] = rnt;
+    }
+    __device__ __forceinline__ void store_current(unsigned char* rec) const {
+        store(rec, cc, edges, am, nt);
+    }
+    // Loads a compact record through L2; degrees are recomputed from the rows.
+    __device__ __forceinline__ void load(const unsigned char* rec) {
+        uint4 h0 = make_uint4(0, 0, 0, 0), h1 = make_uint4(0, 0, 0, 0);
+        if (lane == 0) {
+            h0 = __ldcg(reinterpret_cast<const uint4*>(rec));
+            h1 = __ldcg(reinterpret_cast<const uint4*>(rec) + 1);
+        }
+        const uint4 rr = __ldcg(reinterpret_cast<const uint4*>(rec + 32) + lane);
+        ids = __ldcg(reinterpret_cast<const uint32_t*>(rec + 32 + 512) + lane);
+        nt = __ldcg(reinterpret_cast<const uint32_t*>(rec + 32 + 512 + 128) + lane);
+        cc = __shfl_sync(FULL, h0.x, 0);
+        edges = __shfl_sync(FULL, h0.y, 0);
+        am = ((unsigned long long)__shfl_sync(FULL, h1.y, 0) << 32) | __shfl_sync(FULL, h1.x, 0);
+        r[0] = ((unsigned long long)rr.y << 32) | rr.x;
+        r[1] = ((unsigned long long)rr.w << 32) | rr.z;
+        set_alive_and_degrees();
+        doom = false;
+    }
+    __device__ __forceinline__ void set_alive_and_degrees() {
+        alv = 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            alv |= ((uint32_t)(am >> (32 * i + lane)) & 1u) << i;
+            d[i] = __popcll(r[i] & am);
+        }
+    }
+    // Renumbers a reduced wide node with at most 64 alive vertices. `sb` is the warp's shared
+    // scratch (at least 64 u16 + W words).
+    template <int W, bool I2>
+    __device__ __forceinline__ void from_wide(const WarpNode<W, I2>& w, uint32_t* sb) {
+        lane = w.lane;
+        cc = w.cc;
+        edges = w.edges;
+        doom = false;
+        // slot of an alive vertex 32j + b: (alive before word j) + (alive below b in word j)
+        const uint32_t pc = lane < W ? __popc(w.aw) : 0u;
+        uint32_t incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t base = incl - pc;  // lane j < W: first slot of word j
+        uint16_t* sid = reinterpret_cast<uint16_t*>(sb);
+        const uint32_t nalive = __shfl_sync(FULL, incl, 31);
+        if (lane < 64 - 32) {
+            sid[lane] = 0xFFFFu;
+            sid[lane + 32] = 0xFFFFu;
+        }
+        __syncwarp();
+        // vertex 32 i + lane (alive bit i of this lane) → slot
+#pragma unroll 1
+        for (int i = 0; i < W; ++i) {
+            const uint32_t awi = __shfl_sync(FULL, w.aw, i);
+            const uint32_t bi = __shfl_sync(FULL, base, i);
+            if ((w.alv >> i) & 1u) sid[bi + __popc(awi & ((1u << lane) - 1u))] = (uint16_t)(32 * i + lane);
+        }
+        __syncwarp();
+        const uint32_t id0 = sid[lane], id1 = sid[lane + 32];
+        ids = id0 | (id1 << 16);
+        am = nalive >= 64 ? ~0ull : ((1ull << nalive) - 1ull);
+        nt = 0;  // (verdicts are a cache: starting empty only re-runs tests)
+        // induced rows: compress row(id) over the alive set, word by word
+        r[0] = r[1] = 0;
+#pragma unroll 1
+        for (int j = 0; j < W; ++j) {
+            const uint32_t awj = __shfl_sync(FULL, w.aw, j);
+            const uint32_t bj = __shfl_sync(FULL, base, j);
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const uint32_t id = h ? id1 : id0;
+                if (id == 0xFFFFu) continue;
+                uint32_t m = w.row_word(id, j) & awj;
+                while (m) {
+                    const uint32_t b = __ffs(m) - 1;
+                    m &= m - 1;
+                    r[h] |= 1ull << (bj + __popc(awj & ((1u << b) - 1u)));
+                }
+            }
+        }
+        set_alive_and_degrees();
+    }
+    // Word `lane` (< W) of the cover bitmap (vertices not alive), built in shared scratch.
+    template <int W>
+    __device__ __forceinline__ uint32_t cover_word(uint32_t* sb) const {
+        if (lane < W) sb[lane] = FULL;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const uint32_t id = (ids >> (16 * i)) & 0xFFFFu;
+            if (alive(i)) atomicAnd(&sb[id >> 5], ~(1u << (id & 31)));
+        }
+        __syncwarp();
+        const uint32_t w = lane < W ? sb[lane] : 0u;
+        __syncwarp();
+        return w;
+    }
+};
+
+// reduce_loop (reductions.cpp:63-90) on either node layout: rounds of {degree-one,
+// degree-two-triangle, high-degree} passes, each an ascending scan acting at visit time
+// (first_in: the next candidate >= pos at this moment), until a round changes nothing.
+template <class N, class Cnt>
+__device__ __forceinline__ void reduce_node(N& x, int pvc, uint32_t k, uint32_t snap, Cnt& st) {
+    while (x.edges != 0) {
+        ++st.rounds;
+        // Doom test at every round start (see pass 3): a node loaded from a record is usually
+        // decided here, before any rule runs.
+        const uint32_t lim0 = limit_for(pvc, k, snap, x.cc);
+        const uint32_t above = x.above_mask(lim0);
+        if (__reduce_add_sync(FULL, __popc(above)) > lim0) {
+            x.doom = true;
+            return;
+        }
+        // Candidate masks of the three passes at round start; they stay exact until the next
+        // removal, so a pass without candidates is skipped and the first scan of a pass reuses
+        // its mask.
+        uint32_t m1, m2;
+        x.deg_masks(m1, m2);
+        if (!__any_sync(FULL, (m1 | m2 | above) != 0)) break;  // the final no-change round
+        bool removed = false;  // a removal happened since the round-start masks
+        bool changed = false;
+#pragma unroll 1
+        for (int pass = 1; pass <= 3; ++pass) {
+            long long t0 = N::kInstr ? clock64() : 0;
+            uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
+            uint32_t cand = pass == 1 ? m1 : pass == 2 ? m2 : above;
+            bool stale = removed;  // cand must be recomputed before use
+            if (pass == 3) {
+                const uint32_t lim = limit_for(pvc, k, snap, x.cc);
+                // Every alive vertex above the limit at pass start is removed by this pass (each
+                // removal lowers the limit by one and any degree by at most one), so more than
+                // `lim` of them take |S| past the bound: the node is pruned.
+                if (removed) {  // (otherwise lim == lim0 and the round-start test holds)
+                    cand = x.above_mask(lim);
+                    if (__reduce_add_sync(FULL, __popc(cand)) > lim) x.doom = true;
+                    stale = false;
+                }
+                c = lim;
+            }
+            if (!stale && !__any_sync(FULL, cand != 0)) continue;
+            int pos = 0;
+#pragma unroll 1
+            while (!x.doomed(pvc, k, snap)) {
+                // (a degree-two vertex already known not to close a triangle is skipped: its
+                // partners are unchanged while its degree is, so the test would fail)
+                if (stale) {
+                    cand = (pass == 3 ? x.above_mask(c) : x.eq_mask(c)) & ~(pass == 2 ? x.nt : 0u);
+                    stale = false;
+                }
+                const int v = x.first_in(cand, pos);
+                if (v < 0) break;
+                pos = v + 1;
+                int u0 = v, u1 = -1;
+                if (pass < 3) {
+                    int p0, p1;
+                    x.first_neighbors(v, p0, p1);
+                    u0 = p0;  // degree one: its unique alive neighbour (reductions.cpp:7-19)
+                    if (pass == 2) {  // degree two: both partners iff adjacent (:22-40)
+                        const bool tri = x.is_edge(p0, p1);
+                        u0 = tri ? p0 : -1;
+                        u1 = tri ? p1 : -1;
+                        if (!tri) x.mark_nt(v);
+                    }
+                }
+#pragma unroll 1
+                for (int t = 0; t < 2; ++t) {
+                    const int u = t ? u1 : u0;
+                    if (u < 0) break;
+                    x.remove_vertex((uint32_t)u);
+                    changed = true;
+                    removed = stale = true;
+                    st.rm1 += pass == 1;
+                    st.rm2 += pass == 2;
+                    st.rmh += pass == 3;
+                }
+                if (pass == 3) c = limit_for(pvc, k, snap, x.cc);  // :50-56
+            }
+            if (N::kInstr) st.phase[PH_DEG1 + pass - 1] += clock64() - t0;
+            if (x.doomed(pvc, k, snap)) return;
+        }
+        if (!changed) break;
+    }
+}
+
+template <int W, bool INSTR>
+template <class Cnt>
+__device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int pvc, uint32_t k, uint32_t snap,
+                                                           Cnt& st) {
+    reduce_node(*this, pvc, k, snap, st);
+}
+template <bool INSTR>
+template <class Cnt>
+__device__ __forceinline__ void CompactNode<INSTR>::reduce(int pvc, uint32_t k, uint32_t snap,
+                                                           Cnt& st) {
+    reduce_node(*this, pvc, k, snap, st);
+}
+
 // ------------------------------------------------------------------ device worklist
 
 // GlobalWorklist::try_add (worklist.cpp:11-19): reserve capacity in the packed word (also
@@ -628,10 +896,21 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
 
 // ------------------------------------------------------------------ the traversal kernel
 
+// Copies one node record (either layout) through L2: `vec16` 16-byte vectors spread over the
+// warp's lanes.
+__device__ __forceinline__ void copy_record_raw(const unsigned char* src, unsigned char* dst,
+                                                uint32_t vec16, int lane) {
+#pragma unroll 1
+    for (uint32_t t = lane; t < vec16; t += 32)
+        reinterpret_cast<uint4*>(dst)[t] = __ldcg(reinterpret_cast<const uint4*>(src) + t);
+}
+
+enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
+
 template <int W, bool INSTR>
 #ifndef VCG_MINB16
-#define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
-#endif               // (C5 now: 3 → 80 regs, 26.6 ms; 4 → 64 regs + spills, 28.0 ms)
+#define VCG_MINB16 2  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#endif               // (with the compact layout: 2 → 128 regs, C5 12.5 ms; 3 → 80 + spills, 13.1)
 #ifndef VCG_MINB8
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
@@ -648,9 +927,16 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
 
     const unsigned long long t_start = globaltimer();
     const long long c_start = clock64();
+    // The current node is WIDE (x: all 32*W vertex slots) until at most 64 vertices are alive,
+    // then COMPACT (y: renumbered induced subgraph, see CompactNode).
     WarpNode<W, INSTR> x;
     x.ssb = dense_scratch_base<W>(wib);
     x.lane = lane;
+    CompactNode<INSTR> y;
+    y.lane = lane;
+    bool compact = false;
+    uint32_t* const sb = reinterpret_cast<uint32_t*>(dense_smem) + x.ssb;  // warp scratch
+    const uint32_t vec16 = (uint32_t)(a.entry_bytes / 16);
     Counters32 st;
     Ctl* ctl = a.ctl;
     WStats* const my_stats = a.stats + worker;
@@ -668,6 +954,132 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
     uint32_t qsize = 0, polls = kPoll - 1;  // (the first node polls)
+    bool poll = false;
+    uint4 h = make_uint4(0, 0, 0, 0);
+    unsigned long long hw = 0;
+
+    // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
+    auto settle = [&](auto& n) -> int {
+        n.reduce(a.pvc, a.k, best, st);
+        if (poll) {
+            if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
+            if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
+            qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+        }
+        const bool prune = n.doom || should_prune(a.pvc, a.k, best, n.cc, n.edges);
+        st.dooms += n.doom;
+        if (prune) return ACT_POP;
+        if (n.edges == 0) {
+            // record_cover (scheduler.cpp:84-108)
+            uint32_t record = 0;
+            if (lane == 0) {
+                if (a.pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
+                else record = n.cc < atomicMin(&ctl->best, n.cc);
+            }
+            if (__shfl_sync(FULL, record, 0)) {
+                const uint32_t wbits = n.template cover_word<W>(sb);
+                if (lane < W) a.cover_slots[(unsigned long long)worker * W + lane] = wbits;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                    atomicMin(&ctl->best_owner, ((unsigned long long)n.cc << 32) | worker);
+                    if (a.pvc) atomicExch(&ctl->cancel, 1u);
+                    if (a.mailbox) {
+                        a.mailbox[2] = n.cc;
+                        if (a.pvc) a.mailbox[3] = 1;
+                    }
+                }
+            }
+            if (a.pvc) return ACT_BREAK;  // the search is ended (solver_seq.cpp:108)
+            best = min(best, n.cc);
+            return ACT_POP;
+        }
+        return ACT_BRANCH;
+    };
+
+    // Branch (scheduler.cpp:185-203) on the smallest-id max-degree vertex v: defer remove-N(v)
+    // — donated while the worklist is below its threshold (with donate_oldest the oldest stacked
+    // node goes instead and the child is stacked) — and continue with remove-v.
+    auto branch = [&](auto& n) -> int {
+        long long tm = INSTR ? clock64() : 0;
+        const uint32_t v = n.argmax();
+        ++st.maxdeg;
+        if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
+        long long tb = INSTR ? clock64() : 0;
+        // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
+        // child (0 = remove v_max, 1 = remove N(v_max), scheduler.cpp:303-309), nothing deferred
+        const bool replaying = a.stackonly && replay < a.depth;
+        const bool right = replaying && ((subtree >> replay) & 1ull);
+        replay += replaying;
+        unsigned char* child = nullptr;
+        unsigned long long* publish = nullptr;
+        unsigned long long pos = 0;
+        // (After a full reduction every alive degree is within the high-degree limit, so
+        // |S| + |N(v)| stays below the bound: the deferred child is never dead on arrival.)
+        typename std::remove_reference<decltype(n)>::type::Child c;
+        n.child_begin(v, c);
+        const bool build = !replaying || right;
+        bool dead = false;
+        if (build) {
+            // A child pruned whatever happens is not stored, queued and reloaded: it is counted
+            // as visited right here (the reference counts it when it pops it). The one-worker
+            // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
+            // budget) must not count it — so they stack a 16-byte marker in its place instead.
+            dead = n.template child_pass<true>(c, a.pvc, a.k, best);
+            if (!a.seq_mode) {
+                st.nodes += dead;
+                st.dooms += dead;
+            }
+        }
+        const bool oldest = a.donate_oldest && sp > 0;
+        if (!a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
+            unsigned long long seen = 0;
+            int ok = 0;
+            if (lane == 0) ok = q_reserve(a, pos, seen);
+            if (__shfl_sync(FULL, ok, 0)) {
+                pos = __shfl_sync(FULL, pos, 0);
+                publish = a.seq + (pos & a.ring_mask);
+                if (lane == 0) {
+                    st.max_queue = max(st.max_queue, (uint32_t)seen);
+                    // the slot is free once the previous lap's reader released it
+                    while (ld_acquire_u64(publish) != pos) __nanosleep(32);
+                }
+                __syncwarp();
+                unsigned char* dst = a.wl + (pos & a.ring_mask) * a.entry_bytes;
+                if (oldest) {
+                    copy_record_raw(slot_at(0), dst, vec16, lane);
+                    base = base + 1 == a.stack_bound ? 0 : base + 1;
+                    --sp;
+                } else {
+                    child = dst;
+                }
+                ++st.donated;
+            }
+        }
+        if (build && (!dead || a.seq_mode)) {
+            if (!child) {
+                child = slot_at(sp);
+                ++sp;
+                if (sp > st.high_water) st.high_water = sp;
+            }
+            if (dead) {
+                if (lane == 0) *reinterpret_cast<uint4*>(child) = make_uint4(DEAD_NODE, 0u, 0u, 0u);
+            } else {
+                n.child_store(c, child);
+                ++st.children;
+            }
+        }
+        if (publish) {
+            __syncwarp();  // (the release by lane 0 is cumulative over the warp's stores)
+            if (lane == 0) st_release_u64(publish, pos + 1);
+        }
+        if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
+        if (right) return ACT_POP;  // replay continues with the remove-N(v) child just stacked
+        long long tv = INSTR ? clock64() : 0;
+        n.remove_vertex(v);
+        if (INSTR) st.phase[PH_BRANCH_V] += clock64() - tv;
+        return ACT_CONT;
+    };
 
 #pragma unroll 1
     while (true) {
@@ -728,7 +1140,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 src = a.wl + (pos & a.ring_mask) * a.entry_bytes;
                 idle = false;
             }
-            x.load(src);
+            uint32_t kind = 0;
+            if (lane == 0) kind = __ldcg(reinterpret_cast<const uint32_t*>(src) + 2);
+            compact = __shfl_sync(FULL, kind, 0) == REC_COMPACT;
+            if (compact) y.load(src);
+            else x.load(src);
             if (release) {
                 // every lane's read of the slot is ordered before lane 0's release by the
                 // warp barrier (cumulativity): no full fence needed
@@ -742,16 +1158,12 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             if (INSTR) st.phase[release ? PH_WL_REMOVE : PH_STACK] += clock64() - t0;
         }
 
-        // Issue the read of the hot control line now, consume it after the reduction (its L2
-        // latency hides behind the rule passes). The rules use the bound seen at the previous
-        // node (a stale, larger bound only prunes less).
         // Every worker polling the one control line at every node queues thousands of reads on
         // one L2 slice (and the scoreboard wait lands inside the reduction), so it is polled
         // every kPoll nodes; in between the warp uses the last bound / queue size it saw (a
-        // stale bound only prunes less; the queue size only steers donation).
-        const bool poll = (++polls & (kPoll - 1)) == 0;
-        uint4 h = make_uint4(0, 0, 0, 0);
-        unsigned long long hw = 0;
+        // stale bound only prunes less; the queue size only steers donation). The read is
+        // issued here and consumed after the reduction.
+        poll = (++polls & (kPoll - 1)) == 0;
         if (poll && lane == 0) {
             h = ld_volatile_v4(ctl);
             hw = ld_relaxed_u64(&ctl->work);
@@ -777,135 +1189,24 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             if (__shfl_sync(FULL, stop, 0)) break;
         }
 
-        if (x.cc == DEAD_NODE) {  // a doomed child's marker: visited (counted above), pruned
+        if ((compact ? y.cc : x.cc) == DEAD_NODE) {  // a doomed child's marker: visited, pruned
             ++st.dooms;
             have = false;
             continue;
         }
-        // process_node (scheduler.cpp:125-144)
-        x.reduce(a.pvc, a.k, best, st);
-        if (poll) {
-            if (__shfl_sync(FULL, h.y, 0)) break;
-            if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
-            qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
-        }
-        const bool prune = x.doom || should_prune(a.pvc, a.k, best, x.cc, x.edges);
-        st.dooms += x.doom;
-        if (prune) {
-            have = false;
-            continue;
-        }
-        if (x.edges == 0) {
-            // record_cover (scheduler.cpp:84-108)
-            uint32_t record = 0;
-            if (lane == 0) {
-                if (a.pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
-                else record = x.cc < atomicMin(&ctl->best, x.cc);
-            }
-            if (__shfl_sync(FULL, record, 0)) {
-                const uint32_t wbits = x.cover_word();
-                if (lane < W) a.cover_slots[(unsigned long long)worker * W + lane] = wbits;
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) {
-                    atomicMin(&ctl->best_owner, ((unsigned long long)x.cc << 32) | worker);
-                    if (a.pvc) atomicExch(&ctl->cancel, 1u);
-                    if (a.mailbox) {
-                        a.mailbox[2] = x.cc;
-                        if (a.pvc) a.mailbox[3] = 1;
-                    }
-                }
-            }
-            if (a.pvc) break;  // the search is ended (solver_seq.cpp:108)
-            best = min(best, x.cc);
-            have = false;
-            continue;
-        }
-        long long tm = INSTR ? clock64() : 0;
-        const uint32_t v = x.argmax();
-        ++st.maxdeg;
-        if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
-
-        // Branch (scheduler.cpp:185-203): defer remove-N(v) — donated while the worklist is
-        // below its threshold (with donate_oldest the oldest stacked node goes instead and the
-        // child is stacked) — and continue with remove-v.
-        long long tb = INSTR ? clock64() : 0;
-        // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
-        // child (0 = remove v_max, 1 = remove N(v_max), scheduler.cpp:303-309), nothing deferred
-        const bool replaying = a.stackonly && replay < a.depth;
-        const bool right = replaying && ((subtree >> replay) & 1ull);
-        replay += replaying;
-        unsigned char* child = nullptr;
-        unsigned long long* publish = nullptr;
-        unsigned long long pos = 0;
-        // (After a full reduction every alive degree is within the high-degree limit, so
-        // |S| + |N(v)| stays below the bound: the deferred child is never dead on arrival.)
-        const uint32_t xl = x.branch_mask(v);
-        const uint32_t xcnt = __reduce_add_sync(FULL, __popc(xl));
-        const bool build = !replaying || right;
-        uint32_t keepm = 0;
-        bool dead = false;
-        if (build) {
-            // A child pruned whatever happens is not stored, queued and reloaded: it is counted
-            // as visited right here (the reference counts it when it pops it). The one-worker
-            // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
-            // budget) must not count it — so they stack a 16-byte marker in its place instead.
-            dead = x.template child_pass<true>(xl, xcnt, a.pvc, a.k, best, keepm);
-            if (!a.seq_mode) {
-                st.nodes += dead;
-                st.dooms += dead;
+        int act;
+        if (compact) {
+            act = settle(y);
+        } else {
+            act = settle(x);
+            if (act == ACT_BRANCH && a.compact && x.alive_count() <= kCompactSlots) {
+                y.from_wide(x, sb);
+                compact = true;
             }
         }
-        const bool oldest = a.donate_oldest && sp > 0;
-        if (!a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
-            unsigned long long seen = 0;
-            int ok = 0;
-            if (lane == 0) ok = q_reserve(a, pos, seen);
-            if (__shfl_sync(FULL, ok, 0)) {
-                pos = __shfl_sync(FULL, pos, 0);
-                publish = a.seq + (pos & a.ring_mask);
-                if (lane == 0) {
-                    st.max_queue = max(st.max_queue, (uint32_t)seen);
-                    // the slot is free once the previous lap's reader released it
-                    while (ld_acquire_u64(publish) != pos) __nanosleep(32);
-                }
-                __syncwarp();
-                unsigned char* dst = a.wl + (pos & a.ring_mask) * a.entry_bytes;
-                if (oldest) {
-                    x.copy_record(slot_at(0), dst);
-                    base = base + 1 == a.stack_bound ? 0 : base + 1;
-                    --sp;
-                } else {
-                    child = dst;
-                }
-                ++st.donated;
-            }
-        }
-        if (build && (!dead || a.seq_mode)) {
-            if (!child) {
-                child = slot_at(sp);
-                ++sp;
-                if (sp > st.high_water) st.high_water = sp;
-            }
-            if (dead) {
-                if (lane == 0) *reinterpret_cast<uint2*>(child) = make_uint2(DEAD_NODE, 0u);
-            } else {
-                x.store_child(keepm, xcnt, child);
-                ++st.children;
-            }
-        }
-        if (publish) {
-            __syncwarp();  // (the release by lane 0 is cumulative over the warp's stores)
-            if (lane == 0) st_release_u64(publish, pos + 1);
-        }
-        if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
-        if (right) {  // replay continues with the remove-N(v) child just stacked
-            have = false;
-            continue;
-        }
-        long long tv = INSTR ? clock64() : 0;
-        x.remove_vertex(v);
-        if (INSTR) st.phase[PH_BRANCH_V] += clock64() - tv;
+        if (act == ACT_BRANCH) act = compact ? branch(y) : branch(x);
+        if (act == ACT_BREAK) break;
+        if (act == ACT_POP) have = false;
     }
 
     if (lane == 0) {
