@@ -261,9 +261,21 @@ bool check_invariants(const Graph& g) {
             uint32_t u = g.nbr[i];
             if (u >= g.n || u == v) return false;
             if (i > g.off[v] && g.nbr[i - 1] >= u) return false;
-            if (!g.has_edge(u, v)) return false;
         }
     }
+    // Symmetry (the reference's has_edge(u, v) for every slot) in one O(m) sweep: with sorted
+    // duplicate-free slices, visiting v in ascending order must meet each u's slice entries in
+    // order, so slot (v, u) matches the next unmatched entry of u's slice and every slice is
+    // consumed exactly.
+    std::vector<uint64_t> cur(g.off.begin(), g.off.end() - 1);
+    for (uint32_t v = 0; v < g.n; ++v)
+        for (uint64_t i = g.off[v]; i < g.off[v + 1]; ++i) {
+            const uint32_t u = g.nbr[i];
+            if (cur[u] >= g.off[u + 1] || g.nbr[cur[u]] != v) return false;
+            ++cur[u];
+        }
+    for (uint32_t u = 0; u < g.n; ++u)
+        if (cur[u] != g.off[u + 1]) return false;
     return true;
 }
 

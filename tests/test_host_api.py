@@ -161,6 +161,18 @@ def test_graph_equality_and_invariants():
     bad[0], bad[1] = bad[1], bad[0]  # unsorted slice
     with pytest.raises(ValueError):
         vc.from_csr(a.num_vertices, a.num_edges, off, bad)
+    # asymmetric: vertex 0 lists 1, 4, 5; retarget its last slot to 6 (sorted, but 6 does not
+    # list 0 and 5 now has one entry too many)
+    asym = nbr.copy()
+    assert list(asym[off[0]:off[1]]) == [1, 4, 5]
+    asym[off[1] - 1] = 6
+    with pytest.raises(ValueError):
+        vc.from_csr(a.num_vertices, a.num_edges, off, asym)
+    # a self-loop / out-of-range id
+    loop = nbr.copy()
+    loop[off[1] - 1] = 0
+    with pytest.raises(ValueError):
+        vc.from_csr(a.num_vertices, a.num_edges, off, loop)
 
 
 # ---- host seed and oracle functions vs the reference's golden answers ---------------------
