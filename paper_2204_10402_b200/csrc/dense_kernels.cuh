@@ -145,6 +145,21 @@ __device__ __forceinline__ bool should_prune(int pvc, uint32_t k, uint32_t best,
     return (unsigned long long)edges > s * s;
 }
 
+// The bound B of a search: a node is pruned once |S| > B (PVC: B = k; MVC: B = best - 1), and
+// ReductionBound::current (reductions.hpp:19-27) and should_prune (bounds.cpp:21-30) are both
+// functions of B - |S| alone — one code path for both modes, no per-node mode branches.
+__device__ __forceinline__ int bound_of(int pvc, uint32_t k, uint32_t best) {
+    return pvc ? (int)k : (int)best - 1;
+}
+__device__ __forceinline__ uint32_t limit_of(int B, uint32_t cc) {
+    return B > (int)cc ? (uint32_t)(B - (int)cc) : 0u;
+}
+__device__ __forceinline__ bool prune_at(int B, uint32_t cc, uint32_t edges) {
+    if ((int)cc > B) return true;
+    const unsigned long long s = (uint32_t)(B - (int)cc);
+    return (unsigned long long)edges > s * s;
+}
+
 // Host mailbox (pinned, mapped): one poller per device (worker 0) folds an external MVC bound
 // into the device bound and turns a host cancel request into the device cancel flag.
 __device__ __noinline__ void poll_mailbox(volatile uint32_t* mb, int pvc, Ctl* ctl) {
@@ -325,13 +340,17 @@ struct WarpNode {
     }
     // A node whose cover reaches the bound is pruned whatever the remaining rules do
     // (should_prune tests |S| first and rules only grow S), so the reduction may stop there.
-    __device__ __forceinline__ bool doomed(int pvc, uint32_t k, uint32_t snap) const {
-        return doom || (pvc ? cc > k : cc >= snap);
-    }
+    __device__ __forceinline__ bool doomed(int B) const { return doom || (int)cc > B; }
 
-    // reduce_loop (reductions.cpp:63-90), shared with the compact node (reduce_node below)
+    // reduce_loop (reductions.cpp:63-90), shared with the compact node (reduce_node below).
+    // Candidate masks are bit-sliced per lane (bit i = vertex 32*i + lane).
+    using Mask = uint32_t;
+    __device__ __forceinline__ static bool any(Mask m) { return __any_sync(FULL, m != 0); }
+    __device__ __forceinline__ static uint32_t count(Mask m) {
+        return __reduce_add_sync(FULL, __popc(m));
+    }
     template <class Cnt>
-    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st);
+    __device__ __forceinline__ void reduce(int B, Cnt& st);
     // candidate masks of passes 1 and 2 (alive, degree one / degree two without a cached
     // non-triangle verdict)
     __device__ __forceinline__ void deg_masks(uint32_t& m1, uint32_t& m2) const {
@@ -371,8 +390,8 @@ struct WarpNode {
         c.xcnt = __reduce_add_sync(FULL, __popc(c.xl));
     }
     template <bool TEST>
-    __device__ __forceinline__ bool child_pass(Child& c, int pvc, uint32_t k, uint32_t snap) const {
-        return child_pass<TEST>(c.xl, c.xcnt, pvc, k, snap, c.keepm);
+    __device__ __forceinline__ bool child_pass(Child& c, int B) const {
+        return child_pass<TEST>(c.xl, c.xcnt, B, c.keepm);
     }
     __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
         store_child(c.keepm, c.xcnt, rec);
@@ -384,7 +403,7 @@ struct WarpNode {
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
         uint32_t keepm;
-        (void)child_pass<false>(xl, xcnt, 0, 0, 0, keepm);
+        (void)child_pass<false>(xl, xcnt, 0, keepm);
         store_child(keepm, xcnt, rec);
     }
     // The popcount pass of the remove-N(v) child: for every survivor w, the degree it loses,
@@ -395,8 +414,8 @@ struct WarpNode {
     // bound it would see at best) — and stops as soon as the count passes the limit. Returns
     // true for such a dead child (scratch is then incomplete).
     template <bool TEST>
-    __device__ __forceinline__ bool child_pass(uint32_t xl, uint32_t xcnt, int pvc, uint32_t k,
-                                               uint32_t snap, uint32_t& keep_out) const {
+    __device__ __forceinline__ bool child_pass(uint32_t xl, uint32_t xcnt, int B,
+                                               uint32_t& keep_out) const {
         // X in registers on every lane; xm = this lane's vertices that X removes
         uint32_t X[W];
         uint32_t xm = 0;
@@ -410,8 +429,8 @@ struct WarpNode {
         uint32_t lim = 0;
         if (TEST) {
             const uint32_t c2 = cc + xcnt;
-            if (pvc ? c2 > k : c2 >= snap) return true;
-            lim = limit_for(pvc, k, snap, c2);
+            if ((int)c2 > B) return true;
+            lim = limit_of(B, c2);
             // headroom d - lim of the survivors above the child's limit (0: not a candidate);
             // such a survivor stays above iff it loses less than its headroom
 #pragma unroll
@@ -542,25 +561,32 @@ struct WarpNode {
 // the wide layout (and in the reference): node counts are unchanged. The alive set only shrinks,
 // so every descendant of a compact node stays compact with the same slots.
 constexpr uint32_t kCompactSlots = 64;
-// Compact record: {cc, edges, kind, 0, alive lo, alive hi, 0, 0} + per lane {row of slot lane,
-// row of slot lane+32} (16 B) + per lane packed ids (2 x u16) + per lane cached verdicts.
-constexpr uint32_t kCompactRecordBytes = 32 + 32 * 16 + 32 * 4 + 32 * 4;
+// Compact record: {cc, edges, kind, 0, alive lo, alive hi, verdicts lo, verdicts hi} + per lane
+// {row of slot lane, row of slot lane+32} (16 B) + per lane packed ids (2 x u16).
+constexpr uint32_t kCompactRecordBytes = 32 + 32 * 16 + 32 * 4;
 
 template <bool INSTR>
 struct CompactNode {
     static constexpr bool kInstr = INSTR;
     static constexpr int H = 2;          // slots per lane
+    // Candidate masks are WARP-UNIFORM 64-bit slot masks built with two ballots: counting and
+    // "first candidate >= pos" are then plain ALU work on every lane, with no reductions.
+    using Mask = unsigned long long;
     unsigned long long r[H];             // induced row of slot 32*i + lane (bit c: slot c adjacent)
     uint32_t d[H];                       // degree of slot 32*i + lane (meaningless once removed)
-    uint32_t alv;                        // bit i: slot 32*i + lane is alive
-    unsigned long long am;               // alive slots (warp-uniform)
-    uint32_t nt;                         // bit i: cached degree-two non-triangle verdict
+    Mask am;                             // alive slots
+    Mask nt;                             // cached degree-two non-triangle verdicts
     uint32_t ids;                        // vertex ids of slots lane (low 16) and lane + 32 (high)
     uint32_t cc, edges;                  // uniform
     bool doom;                           // uniform
     int lane;
 
-    __device__ __forceinline__ bool alive(int i) const { return (alv >> i) & 1u; }
+    __device__ __forceinline__ static Mask ballot2(bool p0, bool p1) {
+        return ((Mask)__ballot_sync(FULL, p1) << 32) | __ballot_sync(FULL, p0);
+    }
+    __device__ __forceinline__ static bool any(Mask m) { return m != 0; }
+    __device__ __forceinline__ static uint32_t count(Mask m) { return __popcll(m); }
+    __device__ __forceinline__ bool alive(int i) const { return (am >> (32 * i + lane)) & 1ull; }
     // the row of slot u on every lane
     __device__ __forceinline__ unsigned long long row(uint32_t u) const {
         return __shfl_sync(FULL, (u >> 5) ? r[1] : r[0], u & 31);
@@ -570,46 +596,34 @@ struct CompactNode {
         const uint32_t du = __popcll(ru & am);
 #pragma unroll
         for (int i = 0; i < H; ++i) d[i] -= (uint32_t)(ru >> (32 * i + lane)) & 1u;
-        if (lane == (int)(u & 31)) alv &= ~(1u << (u >> 5));
         am &= ~(1ull << u);
         cc += 1;
         edges -= du;
     }
-    __device__ __forceinline__ uint32_t eq_mask(uint32_t c) const {
-        uint32_t m = 0;
-#pragma unroll
-        for (int i = 0; i < H; ++i) m |= (d[i] == c ? 1u : 0u) << i;
-        return m & alv;
+    __device__ __forceinline__ Mask eq_mask(uint32_t c) const {
+        return ballot2(d[0] == c, d[1] == c) & am;
     }
-    __device__ __forceinline__ uint32_t above_mask(uint32_t lim) const {
-        uint32_t m = 0;
-#pragma unroll
-        for (int i = H - 1; i >= 0; --i) m = __funnelshift_l(lim - d[i], m, 1);
-        return m & alv;
+    __device__ __forceinline__ Mask above_mask(uint32_t lim) const {
+        return ballot2(d[0] > lim, d[1] > lim) & am;
     }
-    __device__ __forceinline__ void deg_masks(uint32_t& m1, uint32_t& m2) const {
+    __device__ __forceinline__ void deg_masks(Mask& m1, Mask& m2) const {
         m1 = eq_mask(1u);
         m2 = eq_mask(2u) & ~nt;
     }
-    __device__ __forceinline__ int first_in(uint32_t m, int pos) const {
-        const uint32_t pi = (uint32_t)pos >> 5;
-        m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
-        const uint32_t key = m ? (((uint32_t)__ffs(m) - 1u) << 5) | (uint32_t)lane : FULL;
-        const uint32_t v = __reduce_min_sync(FULL, key);
-        return v == FULL ? -1 : (int)v;
+    __device__ __forceinline__ static int first_in(Mask m, int pos) {
+        m = pos < 64 ? m & (~0ull << pos) : 0ull;
+        return __ffsll((long long)m) - 1;
     }
     __device__ __forceinline__ void first_neighbors(uint32_t v, int& p0, int& p1) const {
         unsigned long long x = row(v) & am;
         p0 = __ffsll((long long)x) - 1;
         x &= x - 1;
-        p1 = x ? __ffsll((long long)x) - 1 : -1;
+        p1 = __ffsll((long long)x) - 1;
     }
     __device__ __forceinline__ bool is_edge(uint32_t p, uint32_t q) const {
         return (row(p) >> q) & 1ull;
     }
-    __device__ __forceinline__ void mark_nt(uint32_t v) {
-        if (lane == (int)(v & 31)) nt |= 1u << (v >> 5);
-    }
+    __device__ __forceinline__ void mark_nt(uint32_t v) { nt |= 1ull << v; }
     __device__ __forceinline__ uint32_t argmax() const {  // search_node.cpp:34-46
         uint32_t mx = 0;
 #pragma unroll
@@ -618,16 +632,14 @@ struct CompactNode {
         mx = __reduce_max_sync(FULL, mx);
         return 2047u - (mx & 2047u);
     }
-    __device__ __forceinline__ bool doomed(int pvc, uint32_t k, uint32_t snap) const {
-        return doom || (pvc ? cc > k : cc >= snap);
-    }
+    __device__ __forceinline__ bool doomed(int B) const { return doom || (int)cc > B; }
     template <class Cnt>
-    __device__ __forceinline__ void reduce(int pvc, uint32_t k, uint32_t snap, Cnt& st);
+    __device__ __forceinline__ void reduce(int B, Cnt& st);
 
     // ---- the remove-N(v) child (search_node.cpp:27-32 on a clone)
     struct Child {
-        unsigned long long X;  // slots the child covers: N(v) ∩ alive
-        uint32_t xcnt, keepm;  // |X|; this lane's surviving slots
+        Mask X;                // slots the child covers: N(v) ∩ alive
+        uint32_t xcnt;         // |X|
         uint32_t nd[H];        // the survivors' degrees in the child
     };
     __device__ __forceinline__ void child_begin(uint32_t v, Child& c) const {
@@ -635,44 +647,36 @@ struct CompactNode {
         c.xcnt = __popcll(c.X);
     }
     // Degrees of the child; with TEST, true if it is pruned whatever happens when visited (its
-    // cover reaches the bound, or more survivors than its limit stay above it — the round-start
+    // cover exceeds the bound, or more survivors than its limit stay above it — the round-start
     // doom test of reduce_node on the child's state).
     template <bool TEST>
-    __device__ __forceinline__ bool child_pass(Child& c, int pvc, uint32_t k, uint32_t snap) const {
-        uint32_t xm = 0;
+    __device__ __forceinline__ bool child_pass(Child& c, int B) const {
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-            xm |= ((uint32_t)(c.X >> (32 * i + lane)) & 1u) << i;
-            c.nd[i] = d[i] - __popcll(r[i] & c.X);
-        }
-        c.keepm = alv & ~xm;
+        for (int i = 0; i < H; ++i) c.nd[i] = d[i] - __popcll(r[i] & c.X);
         if (!TEST) return false;
         const uint32_t c2 = cc + c.xcnt;
-        if (pvc ? c2 > k : c2 >= snap) return true;
-        const uint32_t lim = limit_for(pvc, k, snap, c2);
-        uint32_t above = 0;
-#pragma unroll
-        for (int i = 0; i < H; ++i) above += ((c.keepm >> i) & 1u) && c.nd[i] > lim;
-        return __reduce_add_sync(FULL, above) > lim;
+        if ((int)c2 > B) return true;
+        const uint32_t lim = limit_of(B, c2);
+        return __popcll(ballot2(c.nd[0] > lim, c.nd[1] > lim) & am & ~c.X) > lim;
     }
     __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
+        const Mask keep = am & ~c.X;
         uint32_t esum = 0;
 #pragma unroll
-        for (int i = 0; i < H; ++i) esum += ((c.keepm >> i) & 1u) ? c.nd[i] : 0u;
+        for (int i = 0; i < H; ++i) esum += ((keep >> (32 * i + lane)) & 1ull) ? c.nd[i] : 0u;
         const uint32_t e2 = __reduce_add_sync(FULL, esum);
-        store(rec, cc + c.xcnt, e2 / 2, am & ~c.X, nt & c.keepm);
+        store(rec, cc + c.xcnt, e2 / 2, keep, nt & keep);
     }
     __device__ __forceinline__ void store(unsigned char* rec, uint32_t rcc, uint32_t redges,
-                                          unsigned long long ram, uint32_t rnt) const {
+                                          Mask ram, Mask rnt) const {
         if (lane == 0) {
             reinterpret_cast<uint4*>(rec)[0] = make_uint4(rcc, redges, REC_COMPACT, 0u);
-            reinterpret_cast<uint4*>(rec)[1] =
-                make_uint4((uint32_t)ram, (uint32_t)(ram >> 32), 0u, 0u);
+            reinterpret_cast<uint4*>(rec)[1] = make_uint4((uint32_t)ram, (uint32_t)(ram >> 32),
+                                                          (uint32_t)rnt, (uint32_t)(rnt >> 32));
         }
         reinterpret_cast<uint4*>(rec + 32)[lane] =
             make_uint4((uint32_t)r[0], (uint32_t)(r[0] >> 32), (uint32_t)r[1], (uint32_t)(r[1] >> 32));
         reinterpret_cast<uint32_t*>(rec + 32 + 512)[lane] = ids;
-        reinterpret_cast<uint32_t*>(rec + 32 + 512 + 128)[lane] = rnt;
     }
     __device__ __forceinline__ void store_current(unsigned char* rec) const {
         store(rec, cc, edges, am, nt);
@@ -686,22 +690,18 @@ struct CompactNode {
         }
         const uint4 rr = __ldcg(reinterpret_cast<const uint4*>(rec + 32) + lane);
         ids = __ldcg(reinterpret_cast<const uint32_t*>(rec + 32 + 512) + lane);
-        nt = __ldcg(reinterpret_cast<const uint32_t*>(rec + 32 + 512 + 128) + lane);
         cc = __shfl_sync(FULL, h0.x, 0);
         edges = __shfl_sync(FULL, h0.y, 0);
-        am = ((unsigned long long)__shfl_sync(FULL, h1.y, 0) << 32) | __shfl_sync(FULL, h1.x, 0);
+        am = ((Mask)__shfl_sync(FULL, h1.y, 0) << 32) | __shfl_sync(FULL, h1.x, 0);
+        nt = ((Mask)__shfl_sync(FULL, h1.w, 0) << 32) | __shfl_sync(FULL, h1.z, 0);
         r[0] = ((unsigned long long)rr.y << 32) | rr.x;
         r[1] = ((unsigned long long)rr.w << 32) | rr.z;
-        set_alive_and_degrees();
+        set_degrees();
         doom = false;
     }
-    __device__ __forceinline__ void set_alive_and_degrees() {
-        alv = 0;
+    __device__ __forceinline__ void set_degrees() {
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-            alv |= ((uint32_t)(am >> (32 * i + lane)) & 1u) << i;
-            d[i] = __popcll(r[i] & am);
-        }
+        for (int i = 0; i < H; ++i) d[i] = __popcll(r[i] & am);
     }
     // Renumbers a reduced wide node with at most 64 alive vertices. `sb` is the warp's shared
     // scratch (at least 64 u16 + W words).
@@ -722,10 +722,8 @@ struct CompactNode {
         const uint32_t base = incl - pc;  // lane j < W: first slot of word j
         uint16_t* sid = reinterpret_cast<uint16_t*>(sb);
         const uint32_t nalive = __shfl_sync(FULL, incl, 31);
-        if (lane < 64 - 32) {
-            sid[lane] = 0xFFFFu;
-            sid[lane + 32] = 0xFFFFu;
-        }
+        sid[lane] = 0xFFFFu;
+        sid[lane + 32] = 0xFFFFu;
         __syncwarp();
         // vertex 32 i + lane (alive bit i of this lane) → slot
 #pragma unroll 1
@@ -736,6 +734,7 @@ struct CompactNode {
         }
         __syncwarp();
         const uint32_t id0 = sid[lane], id1 = sid[lane + 32];
+        __syncwarp();
         ids = id0 | (id1 << 16);
         am = nalive >= 64 ? ~0ull : ((1ull << nalive) - 1ull);
         nt = 0;  // (verdicts are a cache: starting empty only re-runs tests)
@@ -757,7 +756,7 @@ struct CompactNode {
                 }
             }
         }
-        set_alive_and_degrees();
+        set_degrees();
     }
     // Word `lane` (< W) of the cover bitmap (vertices not alive), built in shared scratch.
     template <int W>
@@ -780,51 +779,53 @@ struct CompactNode {
 // degree-two-triangle, high-degree} passes, each an ascending scan acting at visit time
 // (first_in: the next candidate >= pos at this moment), until a round changes nothing.
 template <class N, class Cnt>
-__device__ __forceinline__ void reduce_node(N& x, int pvc, uint32_t k, uint32_t snap, Cnt& st) {
+__device__ __forceinline__ void reduce_node(N& x, int B, Cnt& st) {
+    using Mask = typename N::Mask;
     while (x.edges != 0) {
         ++st.rounds;
         // Doom test at every round start (see pass 3): a node loaded from a record is usually
         // decided here, before any rule runs.
-        const uint32_t lim0 = limit_for(pvc, k, snap, x.cc);
-        const uint32_t above = x.above_mask(lim0);
-        if (__reduce_add_sync(FULL, __popc(above)) > lim0) {
+        const uint32_t lim0 = limit_of(B, x.cc);
+        const Mask above = x.above_mask(lim0);
+        if (N::count(above) > lim0) {
             x.doom = true;
             return;
         }
         // Candidate masks of the three passes at round start; they stay exact until the next
         // removal, so a pass without candidates is skipped and the first scan of a pass reuses
         // its mask.
-        uint32_t m1, m2;
+        Mask m1, m2;
         x.deg_masks(m1, m2);
-        if (!__any_sync(FULL, (m1 | m2 | above) != 0)) break;  // the final no-change round
+        if (!N::any(m1 | m2 | above)) break;  // the final no-change round
         bool removed = false;  // a removal happened since the round-start masks
         bool changed = false;
 #pragma unroll 1
         for (int pass = 1; pass <= 3; ++pass) {
             long long t0 = N::kInstr ? clock64() : 0;
             uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
-            uint32_t cand = pass == 1 ? m1 : pass == 2 ? m2 : above;
+            Mask cand = pass == 1 ? m1 : pass == 2 ? m2 : above;
             bool stale = removed;  // cand must be recomputed before use
             if (pass == 3) {
-                const uint32_t lim = limit_for(pvc, k, snap, x.cc);
+                const uint32_t lim = limit_of(B, x.cc);
                 // Every alive vertex above the limit at pass start is removed by this pass (each
                 // removal lowers the limit by one and any degree by at most one), so more than
                 // `lim` of them take |S| past the bound: the node is pruned.
                 if (removed) {  // (otherwise lim == lim0 and the round-start test holds)
                     cand = x.above_mask(lim);
-                    if (__reduce_add_sync(FULL, __popc(cand)) > lim) x.doom = true;
+                    if (N::count(cand) > lim) x.doom = true;
                     stale = false;
                 }
                 c = lim;
             }
-            if (!stale && !__any_sync(FULL, cand != 0)) continue;
+            if (!stale && !N::any(cand)) continue;
             int pos = 0;
 #pragma unroll 1
-            while (!x.doomed(pvc, k, snap)) {
+            while (!x.doomed(B)) {
                 // (a degree-two vertex already known not to close a triangle is skipped: its
                 // partners are unchanged while its degree is, so the test would fail)
                 if (stale) {
-                    cand = (pass == 3 ? x.above_mask(c) : x.eq_mask(c)) & ~(pass == 2 ? x.nt : 0u);
+                    cand = pass == 3 ? x.above_mask(c) : x.eq_mask(c);
+                    if (pass == 2) cand &= ~x.nt;
                     stale = false;
                 }
                 const int v = x.first_in(cand, pos);
@@ -853,10 +854,10 @@ __device__ __forceinline__ void reduce_node(N& x, int pvc, uint32_t k, uint32_t 
                     st.rm2 += pass == 2;
                     st.rmh += pass == 3;
                 }
-                if (pass == 3) c = limit_for(pvc, k, snap, x.cc);  // :50-56
+                if (pass == 3) c = limit_of(B, x.cc);  // :50-56
             }
             if (N::kInstr) st.phase[PH_DEG1 + pass - 1] += clock64() - t0;
-            if (x.doomed(pvc, k, snap)) return;
+            if (x.doomed(B)) return;
         }
         if (!changed) break;
     }
@@ -864,15 +865,13 @@ __device__ __forceinline__ void reduce_node(N& x, int pvc, uint32_t k, uint32_t 
 
 template <int W, bool INSTR>
 template <class Cnt>
-__device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int pvc, uint32_t k, uint32_t snap,
-                                                           Cnt& st) {
-    reduce_node(*this, pvc, k, snap, st);
+__device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int B, Cnt& st) {
+    reduce_node(*this, B, st);
 }
 template <bool INSTR>
 template <class Cnt>
-__device__ __forceinline__ void CompactNode<INSTR>::reduce(int pvc, uint32_t k, uint32_t snap,
-                                                           Cnt& st) {
-    reduce_node(*this, pvc, k, snap, st);
+__device__ __forceinline__ void CompactNode<INSTR>::reduce(int B, Cnt& st) {
+    reduce_node(*this, B, st);
 }
 
 // ------------------------------------------------------------------ device worklist
@@ -953,6 +952,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     unsigned long long subtree = 0;  // StackOnly: current sub-tree id
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
+    int B = bound_of(a.pvc, a.k, best);  // prune once |S| > B
     uint32_t qsize = 0, polls = kPoll - 1;  // (the first node polls)
     bool poll = false;
     uint4 h = make_uint4(0, 0, 0, 0);
@@ -960,13 +960,16 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto settle = [&](auto& n) -> int {
-        n.reduce(a.pvc, a.k, best, st);
+        n.reduce(B, st);
         if (poll) {
             if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
-            if (!a.pvc) best = min(best, __shfl_sync(FULL, h.x, 0));
+            if (!a.pvc) {
+                best = min(best, __shfl_sync(FULL, h.x, 0));
+                B = bound_of(0, 0, best);
+            }
             qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
         }
-        const bool prune = n.doom || should_prune(a.pvc, a.k, best, n.cc, n.edges);
+        const bool prune = n.doom || prune_at(B, n.cc, n.edges);
         st.dooms += n.doom;
         if (prune) return ACT_POP;
         if (n.edges == 0) {
@@ -992,6 +995,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             }
             if (a.pvc) return ACT_BREAK;  // the search is ended (solver_seq.cpp:108)
             best = min(best, n.cc);
+            B = bound_of(0, 0, best);
             return ACT_POP;
         }
         return ACT_BRANCH;
@@ -1025,7 +1029,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             // as visited right here (the reference counts it when it pops it). The one-worker
             // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
             // budget) must not count it — so they stack a 16-byte marker in its place instead.
-            dead = n.template child_pass<true>(c, a.pvc, a.k, best);
+            dead = n.template child_pass<true>(c, B);
             if (!a.seq_mode) {
                 st.nodes += dead;
                 st.dooms += dead;
@@ -1253,9 +1257,10 @@ __global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
 #pragma unroll 1
     for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < a.count; i += warps) {
         x.load(a.in + (unsigned long long)i * a.entry_bytes);
-        x.reduce(a.pvc, a.k, a.best, st);
+        const int B = bound_of(a.pvc, a.k, a.best);
+        x.reduce(B, st);
         uint32_t flag;
-        if (x.doom || should_prune(a.pvc, a.k, a.best, x.cc, x.edges)) {
+        if (x.doom || prune_at(B, x.cc, x.edges)) {
             flag = 0;
         } else if (x.edges == 0) {
             flag = 1;
