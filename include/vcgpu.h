@@ -157,6 +157,7 @@ typedef struct {
     uint32_t kernel_launches;   /* device kernels this solve launched */
     uint64_t phase_cycles[10];  /* Phase order of metrics.hpp:15-26, summed over workers */
     uint64_t active_cycles;     /* summed over workers */
+    uint64_t donated_peer;      /* of `donated`: nodes written into another shard's worklist */
 } vcg_result;
 
 VCG_API void vcg_params_init(vcg_params* p);
@@ -186,6 +187,43 @@ typedef struct {
 VCG_API int vcg_expand_frontier(const vcg_graph* g, const vcg_params* p, uint64_t target,
                                 vcg_frontier* out);
 VCG_API void vcg_frontier_free(vcg_frontier* f);
+
+/* Multi-shard solves with device-to-device work donation (SURVEY.md §8e "exchange step").
+ * A shard is one dense-engine search (n <= 1024, strategy hybrid) on one GPU with its own device
+ * worklist. Linked shards (one per GPU, or several on one device):
+ *   - donate their oldest stacked node straight into the ring of a shard whose worklist is
+ *     below its threshold (remote stores + a system-scope release over NVLink P2P / CUDA IPC);
+ *   - propagate an improved MVC bound with peer atomicMin and a PVC "found" / timeout / budget
+ *     as a cancel store into every shard;
+ *   - terminate together: shard 0 counts the shards whose `pending` (queued + active) is
+ *     non-zero, maintained by whoever moves a shard's pending between 0 and 1.
+ * Replaces the reference's single shared GlobalWorklist (worklist.cpp:11-48) across GPUs.
+ *
+ * open    : validate + greedy + buffers + seeds on p->device (p->seeds = this shard's share;
+ *           with no seeds the shard starts with the root if with_root, else empty).
+ * export  : CUDA IPC handles of the shard's exchange memory (vcg_session_handle_bytes()).
+ * link_ipc: map every other shard's handles (handles = world x handle bytes, in rank order;
+ *           seeds_per_shard = each shard's seed count, root counted as 1).
+ * link_local: link shards opened in this process (same device or P2P-capable devices).
+ * launch  : asynchronous; launch EVERY shard before waiting on any (they finish together).
+ * wait    : blocks; fills the result like vcg_solve, for this shard's part of the search.
+ * On one device, shards must leave room for each other (params.workers), or the later ones
+ * cannot become resident. */
+#define VCG_MAX_SHARDS 16
+typedef struct vcg_session vcg_session;
+VCG_API int vcg_session_open(const vcg_graph* g, const vcg_params* p, int with_root,
+                             vcg_session** out);
+VCG_API size_t vcg_session_handle_bytes(void);
+VCG_API int vcg_session_export(const vcg_session* s, void* handle);
+VCG_API int vcg_session_link_ipc(vcg_session* s, uint32_t world, uint32_t rank,
+                                 const void* handles, const uint64_t* seeds_per_shard);
+VCG_API int vcg_session_link_local(vcg_session* const* shards, uint32_t world);
+VCG_API int vcg_session_launch(vcg_session* s);
+VCG_API int vcg_session_wait(vcg_session* s, vcg_result* out);
+VCG_API void vcg_session_close(vcg_session* s);
+/* Workers (warps) of a full-device dense-engine solve of g on `device` (shards sharing a device
+ * split them through params.workers). */
+VCG_API int vcg_device_workers(const vcg_graph* g, int32_t device, uint32_t* workers);
 
 /* Pinned, device-mapped host words for vcg_params.mailbox (zeroed); n_words >= 4. */
 VCG_API int vcg_mailbox_alloc(uint32_t n_words, uint32_t** out);

@@ -198,6 +198,29 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
            instrument=False, initial_best=0, seeds=None, mailbox=None, raw=False,
            donate_oldest=None, stream=None, engine="auto"):
     """The strategy dispatch of bindings.cpp:60-99, on the GPU through vcg_solve."""
+    p, keep = _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
+                      timeout_s, node_budget, device=device, rules=rules, block_warps=block_warps,
+                      instrument=instrument, initial_best=initial_best, seeds=seeds,
+                      mailbox=mailbox, donate_oldest=donate_oldest, stream=stream, engine=engine)
+    workers = p.workers
+    r = _n.Result()
+    _n.check(_lib.vcg_solve(graph._h, C.byref(p), C.byref(r)))
+    try:
+        out = _result_dict(r)
+    finally:
+        _lib.vcg_result_free(C.byref(r))
+    del keep
+    if raw:
+        return out
+    return make_report(graph, mode, k, strategy, workers if workers else out["num_workers"],
+                       capacity, threshold_fraction, depth, out)
+
+
+def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
+            timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
+            instrument=False, initial_best=0, seeds=None, mailbox=None, donate_oldest=None,
+            stream=None, engine="auto"):
+    """vcg_params for one solve (validated like bindings.cpp:60-99) + the arrays it points to."""
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
     if engine not in _ENGINES:
@@ -236,17 +259,7 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
         p.mailbox = C.cast(mailbox, C.POINTER(C.c_uint32))
     if stream is not None:
         p.stream = C.c_void_p(int(stream))
-    r = _n.Result()
-    _n.check(_lib.vcg_solve(graph._h, C.byref(p), C.byref(r)))
-    try:
-        out = _result_dict(r)
-    finally:
-        _lib.vcg_result_free(C.byref(r))
-    del keep
-    if raw:
-        return out
-    return make_report(graph, mode, k, strategy, workers if workers else out["num_workers"],
-                       capacity, threshold_fraction, depth, out)
+    return p, keep
 
 
 def _array(ptr, count):
@@ -277,6 +290,7 @@ def _result_dict(r):
         engine=int(r.engine), grid_blocks=int(r.grid_blocks), block_threads=int(r.block_threads),
         kernel_launches=int(r.kernel_launches),
         phase_cycles=[int(x) for x in r.phase_cycles], active_cycles=int(r.active_cycles),
+        donated_peer=int(r.donated_peer),
     )
 
 

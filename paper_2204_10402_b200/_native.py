@@ -54,7 +54,7 @@ class Result(C.Structure):
         ("n_padded", C.c_uint32), ("engine", C.c_int32), ("grid_blocks", C.c_uint32),
         ("block_threads", C.c_uint32), ("kernel_launches", C.c_uint32),
         ("phase_cycles", C.c_uint64 * 10),
-        ("active_cycles", C.c_uint64),
+        ("active_cycles", C.c_uint64), ("donated_peer", C.c_uint64),
     ]
 
 
@@ -96,6 +96,15 @@ _SIGS = [
     ("vcg_result_free", None, [C.POINTER(Result)]),
     ("vcg_expand_frontier", C.c_int, [_VP, C.POINTER(Params), C.c_uint64, C.POINTER(Frontier)]),
     ("vcg_frontier_free", None, [C.POINTER(Frontier)]),
+    ("vcg_session_open", C.c_int, [_VP, C.POINTER(Params), C.c_int, C.POINTER(_VP)]),
+    ("vcg_session_handle_bytes", C.c_size_t, []),
+    ("vcg_session_export", C.c_int, [_VP, C.c_void_p]),
+    ("vcg_session_link_ipc", C.c_int, [_VP, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    ("vcg_session_link_local", C.c_int, [C.c_void_p, C.c_uint32]),
+    ("vcg_session_launch", C.c_int, [_VP]),
+    ("vcg_session_wait", C.c_int, [_VP, C.POINTER(Result)]),
+    ("vcg_session_close", None, [_VP]),
+    ("vcg_device_workers", C.c_int, [_VP, C.c_int32, C.POINTER(C.c_uint32)]),
     ("vcg_mailbox_alloc", C.c_int, [C.c_uint32, C.POINTER(C.POINTER(C.c_uint32))]),
     ("vcg_mailbox_free", None, [C.POINTER(C.c_uint32)]),
     ("vcg_device_count", C.c_int, []),

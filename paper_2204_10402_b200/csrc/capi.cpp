@@ -178,43 +178,49 @@ void vcg_params_init(vcg_params* p) {
     p->rules = VCG_RULES_REFERENCE;
 }
 
-int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
-    return guarded([&]() -> int {
-        if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
-        std::memset(out, 0, sizeof(*out));
-        const vcg::Graph& g = gh->g;
-        // validate_config (scheduler.cpp:20-29) + the k >= 1 check (:330)
-        if (p->capacity < 1) return fail(VCG_EINVAL, "worklist_capacity must be >= 1");
-        if (!(p->threshold_fraction > 0.0) || p->threshold_fraction > 1.0)
-            return fail(VCG_EINVAL, "threshold_fraction must be in (0, 1]");
-        if (p->depth < 1 || p->depth > 30)
-            return fail(VCG_EINVAL, "stackonly_depth must be in [1, 30]");
-        if (p->mode == VCG_PVC && p->k < 1) return fail(VCG_EINVAL, "pvc requires k >= 1");
-        if (p->strategy < VCG_HYBRID || p->strategy > VCG_STACKONLY)
-            return fail(VCG_EINVAL, "unknown strategy");
-        if (p->num_seeds && !p->seeds) return fail(VCG_EINVAL, "null seeds");
-        const auto t0 = std::chrono::steady_clock::now();
-        const bool pvc = p->mode == VCG_PVC;
+namespace {
 
-        // greedy seed (scheduler.cpp:333-340), counted in wall_ms like the reference. MVC needs
-        // it as the initial bound before the search starts; PVC only reports its size
-        // (best := k, stack bound min(k, n)), so there it runs on a host thread while the
-        // device searches.
-        auto run_greedy = [&g, out]() {
+// validate_config (scheduler.cpp:20-29) + the k >= 1 check (:330); 0 when valid
+int validate(const vcg_params* p) {
+    if (p->capacity < 1) return fail(VCG_EINVAL, "worklist_capacity must be >= 1");
+    if (!(p->threshold_fraction > 0.0) || p->threshold_fraction > 1.0)
+        return fail(VCG_EINVAL, "threshold_fraction must be in (0, 1]");
+    if (p->depth < 1 || p->depth > 30) return fail(VCG_EINVAL, "stackonly_depth must be in [1, 30]");
+    if (p->mode == VCG_PVC && p->k < 1) return fail(VCG_EINVAL, "pvc requires k >= 1");
+    if (p->strategy < VCG_HYBRID || p->strategy > VCG_STACKONLY)
+        return fail(VCG_EINVAL, "unknown strategy");
+    if (p->num_seeds && !p->seeds) return fail(VCG_EINVAL, "null seeds");
+    return VCG_OK;
+}
+
+// The host half of run_hybrid (scheduler.cpp:328-359) around one device search: the greedy
+// seed (scheduler.cpp:333-340, counted in wall_ms like the reference; MVC needs it as the initial
+// bound, PVC only reports its size, so there it runs on a host thread while the device
+// searches), the engine spec, and finish_run's result (scheduler.cpp:299-324).
+struct HostRun {
+    const vcg::Graph& g;
+    const vcg_params* p;
+    vcg_result* out;
+    bool pvc;
+    std::chrono::steady_clock::time_point t0;
+    vcg::Greedy greedy;
+    std::future<vcg::Greedy> greedy_async;
+    vcg::SolveSpec s;
+
+    HostRun(const vcg::Graph& g_, const vcg_params* p_, vcg_result* out_)
+        : g(g_), p(p_), out(out_), pvc(p_->mode == VCG_PVC), t0(std::chrono::steady_clock::now()) {
+        std::memset(out, 0, sizeof(*out));
+        auto run_greedy = [this]() {
             const auto a = std::chrono::steady_clock::now();
             vcg::Greedy gr = vcg::greedy_approx(g);
             out->greedy_ms =
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
             return gr;
         };
-        vcg::Greedy greedy;
-        std::future<vcg::Greedy> greedy_async;
         if (pvc && g.n > 0)
             greedy_async = std::async(std::launch::async, run_greedy);
         else
             greedy = run_greedy();
-
-        vcg::SolveSpec s;
         s.pvc = pvc;
         s.k = p->k;
         s.strategy = p->strategy;
@@ -241,27 +247,14 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         s.num_seeds = p->num_seeds;
         s.mailbox = p->mailbox;
         s.stream = p->stream;
+    }
+    ~HostRun() {  // the greedy thread never outlives the call, even on a device error
+        if (greedy_async.valid()) greedy_async.wait();
+    }
 
-        vcg::SolveOut r;
-        struct Join {  // the greedy thread never outlives this call, even on a device error
-            std::future<vcg::Greedy>& f;
-            ~Join() {
-                if (f.valid()) f.wait();
-            }
-        } join{greedy_async};
-        if (g.n == 0) {
-            // no vertex: one root visit, nothing to branch on (MVC 0; PVC feasible, empty)
-            r.worker_nodes.assign(1, 1);
-            r.worker_high_water.assign(1, 0);
-            r.found = pvc;
-            r.wl_added = r.wl_removed = 1;
-        } else {
-            vcg::solve_on_device(g, s, r);
-        }
-
+    void finish(vcg::SolveOut& r) {
         if (greedy_async.valid()) greedy = greedy_async.get();
         out->greedy_size = greedy.size;
-
         // finish_run (scheduler.cpp:299-324): certificate in original ids
         const std::vector<uint32_t>* cov = nullptr;
         if (pvc) {
@@ -321,8 +314,131 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         out->kernel_launches = r.launches;
         for (int i = 0; i < 10; ++i) out->phase_cycles[i] = r.phase[i];
         out->active_cycles = r.active_cycles;
+        out->donated_peer = r.donated_peer;
         out->wall_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+}  // namespace
+
+int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
+    return guarded([&]() -> int {
+        if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
+        std::memset(out, 0, sizeof(*out));
+        if (const int e = validate(p)) return e;
+        HostRun h(gh->g, p, out);
+        vcg::SolveOut r;
+        if (gh->g.n == 0) {
+            // no vertex: one root visit, nothing to branch on (MVC 0; PVC feasible, empty)
+            r.worker_nodes.assign(1, 1);
+            r.worker_high_water.assign(1, 0);
+            r.found = h.pvc;
+            r.wl_added = r.wl_removed = 1;
+        } else {
+            vcg::solve_on_device(gh->g, h.s, r);
+        }
+        h.finish(r);
+        return VCG_OK;
+    });
+}
+
+// ------------------------------------------------------------------ multi-shard sessions
+
+struct vcg_session {
+    const vcg_graph* g;
+    vcg_params p;
+    vcg_result* out = nullptr;   // filled by wait
+    std::unique_ptr<HostRun> host;
+    vcg::Session* ses = nullptr;
+    vcg_result scratch;
+    ~vcg_session() {
+        if (ses) vcg::session_close(ses);
+    }
+};
+
+int vcg_session_open(const vcg_graph* gh, const vcg_params* p, int with_root, vcg_session** out) {
+    return guarded([&]() -> int {
+        if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
+        *out = nullptr;
+        if (const int e = validate(p)) return e;
+        if (gh->g.n == 0) return fail(VCG_EINVAL, "multi-shard sessions need a non-empty graph");
+        if (p->strategy != VCG_HYBRID) return fail(VCG_EINVAL, "multi-shard sessions run strategy hybrid/gpu");
+        auto s = std::make_unique<vcg_session>();
+        s->g = gh;
+        s->p = *p;
+        s->host = std::make_unique<HostRun>(gh->g, &s->p, &s->scratch);
+        s->host->s.no_root = p->num_seeds == 0 && !with_root;
+        s->ses = vcg::session_open(gh->g, s->host->s);
+        *out = s.release();
+        return VCG_OK;
+    });
+}
+
+size_t vcg_session_handle_bytes(void) { return vcg::session_handle_bytes(); }
+
+int vcg_session_export(const vcg_session* s, void* handle) {
+    return guarded([&]() -> int {
+        if (!s || !handle) return fail(VCG_EINVAL, "null argument");
+        vcg::session_export(s->ses, handle);
+        return VCG_OK;
+    });
+}
+
+int vcg_session_link_ipc(vcg_session* s, uint32_t world, uint32_t rank, const void* handles,
+                         const uint64_t* seeds_per_shard) {
+    return guarded([&]() -> int {
+        if (!s || !handles || !seeds_per_shard) return fail(VCG_EINVAL, "null argument");
+        if (world < 1 || world > VCG_MAX_SHARDS || rank >= world)
+            return fail(VCG_EINVAL, "bad shard rank / world");
+        vcg::session_link_ipc(s->ses, world, rank, handles, seeds_per_shard);
+        return VCG_OK;
+    });
+}
+
+int vcg_session_link_local(vcg_session* const* shards, uint32_t world) {
+    return guarded([&]() -> int {
+        if (!shards) return fail(VCG_EINVAL, "null argument");
+        if (world < 1 || world > VCG_MAX_SHARDS) return fail(VCG_EINVAL, "bad shard world");
+        std::vector<vcg::Session*> v(world);
+        for (uint32_t i = 0; i < world; ++i) {
+            if (!shards[i]) return fail(VCG_EINVAL, "null shard");
+            v[i] = shards[i]->ses;
+        }
+        vcg::session_link_local(v.data(), world);
+        return VCG_OK;
+    });
+}
+
+int vcg_session_launch(vcg_session* s) {
+    return guarded([&]() -> int {
+        if (!s) return fail(VCG_EINVAL, "null argument");
+        vcg::session_launch(s->ses);
+        return VCG_OK;
+    });
+}
+
+int vcg_session_wait(vcg_session* s, vcg_result* out) {
+    return guarded([&]() -> int {
+        if (!s || !out) return fail(VCG_EINVAL, "null argument");
+        vcg::SolveOut r;
+        vcg::session_wait(s->ses, r);
+        HostRun& h = *s->host;
+        if (h.greedy_async.valid()) h.greedy = h.greedy_async.get();  // (it writes scratch)
+        std::memset(out, 0, sizeof(*out));
+        out->greedy_ms = s->scratch.greedy_ms;
+        h.out = out;
+        h.finish(r);
+        return VCG_OK;
+    });
+}
+
+void vcg_session_close(vcg_session* s) { delete s; }
+
+int vcg_device_workers(const vcg_graph* g, int32_t device, uint32_t* workers) {
+    return guarded([&]() -> int {
+        if (!g || !workers) return fail(VCG_EINVAL, "null argument");
+        *workers = vcg::full_device_workers(g->g, device);
         return VCG_OK;
     });
 }

@@ -244,6 +244,7 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
         out.dooms += hs[w].dooms;
         out.donated += hs[w].donated;
         out.active_cycles += hs[w].active;
+        out.donated_peer += hs[w].peer;
         out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
         for (int p = 0; p < 10; ++p) out.phase[p] += hs[w].phase[p];
     }
@@ -273,174 +274,425 @@ int device_count() {
 
 static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out);
 
-void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
-    if (s.engine == 2 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
-    if (g.n > 1024)
-        throw std::invalid_argument("graph has " + std::to_string(g.n) +
-                                    " vertices; the dense engine handles n <= 1024");
-    const int dev = s.device;
-    int ndev = device_count();
-    if (ndev == 0) throw std::runtime_error("CUDA error: no CUDA device visible");
-    if (dev < 0 || dev >= ndev) throw std::invalid_argument("device ordinal out of range");
-    CUDA_CHECK(cudaSetDevice(dev));
-    DeviceCtx& C = ctx_for(dev);
-    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
-    cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
-
-    const uint32_t W = pick_w(g.n);
-    const uint32_t npad = 32 * W;
-    const size_t entry = dense_record_bytes(W);
-    out.engine = 1;
-    out.degree_bytes = 2;
-    out.n_padded = npad;
-
-    CUDA_CHECK(cudaEventRecord(C.evh, st));
-    // resident graph (adjacency bitmap), uploaded once per device
+namespace {
+// The adjacency bitmap of `g` on `dev`, uploaded once per device (the caller holds the device's
+// solve lock).
+const DeviceGraph& device_graph(const Graph& g, int dev, cudaStream_t st, SolveOut* out) {
     if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
     if (!g.dev[dev]) {
+        const uint32_t W = pick_w(g.n);
         auto dg = std::make_shared<DeviceGraph>();
         dg->device = dev;
         dg->W = W;
-        dg->npad = npad;
-        std::vector<uint32_t> at = build_bitmap(g, W, npad);
+        dg->npad = 32 * W;
+        std::vector<uint32_t> at = build_bitmap(g, W, dg->npad);
         dg->at4_bytes = at.size() * 4;
         CUDA_CHECK(cudaMalloc(&dg->at4, dg->at4_bytes));
         CUDA_CHECK(cudaMemcpyAsync(dg->at4, at.data(), dg->at4_bytes, cudaMemcpyHostToDevice, st));
-        out.h2d_bytes += dg->at4_bytes;
+        // (a pageable source is staged before cudaMemcpyAsync returns: `at` may go)
+        if (out) out->h2d_bytes += dg->at4_bytes;
         g.dev[dev] = dg;
     }
-    const DeviceGraph& dg = *g.dev[dev];
+    return *g.dev[dev];
+}
 
-    // worker grid: one warp per worker
-    const uint32_t block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
-    const uint32_t block = 32 * block_warps;
-    // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + (size_t)block_warps * W * 32 * 4;
-    int per_sm = 1;
-    switch (W) {
-        case 4: per_sm = occupancy<4>(block, smem, s.instrument); break;
-        case 8: per_sm = occupancy<8>(block, smem, s.instrument); break;
-        case 16: per_sm = occupancy<16>(block, smem, s.instrument); break;
-        default: per_sm = occupancy<32>(block, smem, s.instrument); break;
-    }
-    if (per_sm < 1) throw std::runtime_error("CUDA error: dense kernel cannot be resident");
-    uint32_t workers = s.workers;
-    if (s.strategy == 1) workers = 1;
-    if (workers == 0) workers = (uint32_t)C.sms * per_sm * block_warps;
-    const uint32_t grid = (workers + block_warps - 1) / block_warps;
-    out.grid = grid;
-    out.block = block;
+}  // namespace
 
-    // memory: stacks, worklist ring, control, cover slots, stats
-    const uint32_t bound = std::max<uint32_t>(s.stack_bound, 1) + 1;
-    const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(s.capacity, s.num_seeds), 1);
-    if (cap > (1ull << 30)) throw std::invalid_argument("worklist capacity too large");
-    uint64_t ring = 2;
-    while (ring < cap) ring <<= 1;
-    const size_t stack_bytes = (size_t)workers * bound * entry;
-    const size_t wl_bytes = (size_t)ring * entry;
-    unsigned char* stacks = (unsigned char*)C.stacks.get(stack_bytes);
-    unsigned char* wl = (unsigned char*)C.wl.get(wl_bytes);
-    unsigned long long* seq = (unsigned long long*)C.seq.get(ring * 8);
-    const size_t slots_bytes = (((size_t)workers * W * 4) + 255) / 256 * 256;
-    const size_t misc_bytes = sizeof(Ctl) + slots_bytes + (size_t)workers * sizeof(WStats);
-    unsigned char* misc = (unsigned char*)C.misc.get(misc_bytes);
-    Ctl* ctl = reinterpret_cast<Ctl*>(misc);
-    uint32_t* cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
-    WStats* stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
+// One dense-engine solve on one device: prepare (buffers, seeds, kernel arguments), launch, and
+// finish (result assembly). vcg_solve runs the three back to back on the device's reusable
+// arenas under its solve lock; a multi-shard session owns its buffers, links its kernel to the
+// peers' exchange memory between prepare and launch, and launches every shard before any waits.
+struct DenseRun {
+    const Graph& g;
+    SolveSpec s;
+    int dev;
+    DeviceCtx& C;
+    cudaStream_t st = nullptr;
+    bool owned;  // own buffers and events (session) instead of the device arenas
+    std::vector<void*> allocs;
+    void* host = nullptr;
+    size_t host_bytes = 0;
+    cudaEvent_t evh = nullptr, ev0 = nullptr, ev1 = nullptr;
+    std::vector<void*> ipc_opened;
+    PeerRef* peers_dev = nullptr;
+    uint32_t W = 0, npad = 0, block_warps = 0, block = 0, grid = 0, workers = 0, bound = 0;
+    size_t entry = 0, smem = 0, wl_bytes = 0, seq_bytes = 0, misc_bytes = 0;
+    uint64_t ring = 0, cap = 0, nseeds = 0;
+    unsigned char *stacks = nullptr, *wl = nullptr, *misc = nullptr;
+    unsigned long long* seq = nullptr;
+    Ctl* ctl = nullptr;
+    uint32_t* cover_slots = nullptr;
+    WStats* stats = nullptr;
+    DenseArgs a{};
+    Ctl hc{};
+    SolveOut out;
 
-    // initial worklist content: the root (init_root, search_node.cpp:7-14) or the seeds
-    const uint64_t nseeds = s.num_seeds ? s.num_seeds : 1;
-    std::vector<unsigned char> recs(nseeds * entry);
-    if (s.num_seeds) {
-        for (uint64_t i = 0; i < nseeds; ++i) {
-            const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
-            pack_record(W, g.n, r[0], r[1], r + 2, recs.data() + i * entry);
+    DenseRun(const Graph& g_, const SolveSpec& s_, bool owned_)
+        : g(g_), s(s_), dev(s_.device), C(ctx_for(s_.device)), owned(owned_) {}
+    ~DenseRun() {
+        cudaSetDevice(dev);
+        for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+        if (peers_dev) cudaFree(peers_dev);
+        for (void* p : allocs) cudaFree(p);
+        if (host) cudaFreeHost(host);
+        if (owned) {
+            if (evh) cudaEventDestroy(evh);
+            if (ev0) cudaEventDestroy(ev0);
+            if (ev1) cudaEventDestroy(ev1);
+            if (st) cudaStreamDestroy(st);
         }
-    } else {
-        std::vector<uint32_t> deg(g.n);
-        for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
-        pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs.data());
     }
-    Ctl hc;
-    std::memset(&hc, 0, sizeof(hc));
-    hc.best = s.best;
-    hc.head = 0;
-    hc.tail = nseeds;
-    hc.work = (nseeds << 32) | nseeds;
-    hc.best_owner = ~0ull;
-    CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
-    CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
-    init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
-    CUDA_CHECK(cudaGetLastError());
-    out.launches += 2;  // init_seq_kernel + dense_kernel
-    CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
-    out.h2d_bytes += sizeof(hc) + recs.size();
-
-    DenseArgs a;
-    a.at4 = dg.at4;
-    a.n = g.n;
-    a.npad = npad;
-    a.m = (uint32_t)g.m;
-    a.pvc = s.pvc ? 1 : 0;
-    a.k = s.k;
-    a.capacity = (uint32_t)cap;
-    a.ring_mask = (uint32_t)(ring - 1);
-    a.threshold = (uint32_t)std::min<uint64_t>(s.threshold, cap);
-    a.workers = workers;
-    a.stack_bound = bound;
-    a.entry_bytes = entry;
-    a.stacks = stacks;
-    a.wl = wl;
-    a.seq = seq;
-    a.ctl = ctl;
-    a.cover_slots = cover_slots;
-    a.stats = stats;
-    a.node_budget = s.node_budget;
-    a.timeout_ns = s.timeout_s >= 0 ? (unsigned long long)(s.timeout_s * 1e9) : 0ull;
-    if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
-    a.flush_every = 64;
-    if (s.node_budget) a.flush_every = std::max<uint64_t>(1, std::min<uint64_t>(64, s.node_budget / (4ull * workers)));
-    // idle back-off: exponential from 32 ns, capped at backoff_us (at most 2 us on the device —
-    // a polling warp costs one L2 read, an over-sleeping one leaves queued work unclaimed)
-    a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
-    a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
-    a.donate_oldest = s.donate_oldest ? 1 : 0;
-    a.compact = s.engine == 3 ? 0 : 1;
-    a.stackonly = s.strategy == 2 ? 1 : 0;
-    a.depth = s.depth;
-    a.mailbox = s.mailbox;
-
-    CUDA_CHECK(cudaEventRecord(C.ev0, st));
-    const bool I = s.instrument;
-    switch (W) {
-        case 4: I ? launch_dense<4, true>(a, grid, block, smem, st) : launch_dense<4, false>(a, grid, block, smem, st); break;
-        case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
-        case 16: I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st); break;
-        default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
+    void* dalloc(Arena& arena, size_t bytes) {
+        if (!owned) return arena.get(bytes);
+        void* p = nullptr;
+        CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        allocs.push_back(p);
+        return p;
     }
-    const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
-    out.status = hc.status;
-    out.wl_added = hc.tail;  // every enqueue ticket is one added node (root/seeds included)
-    out.wl_current = (uint32_t)hc.work;
-    out.wl_removed = hc.tail - out.wl_current;
-    out.wl_max_size = nseeds;
-    aggregate(hs, workers, out);
-    if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
-    if (hc.best_owner != ~0ull) {
-        const uint32_t owner = (uint32_t)(hc.best_owner & 0xFFFFFFFFu);
-        out.found = true;
-        out.found_size = (uint32_t)(hc.best_owner >> 32);
-        std::vector<uint32_t> bits(W);
-        CUDA_CHECK(cudaMemcpy(bits.data(), cover_slots + (size_t)owner * W, W * 4, cudaMemcpyDeviceToHost));
-        out.d2h_bytes += W * 4;
-        out.cover.clear();
-        for (uint32_t v = 0; v < g.n; ++v)
-            if ((bits[v >> 5] >> (v & 31)) & 1u) out.cover.push_back(v);
+    void* halloc(size_t bytes) {
+        if (!owned) return C.host.get(bytes);
+        if (bytes > host_bytes) {
+            if (host) CUDA_CHECK(cudaFreeHost(host));
+            host = nullptr;
+            CUDA_CHECK(cudaHostAlloc(&host, bytes, cudaHostAllocDefault));
+            host_bytes = bytes;
+        }
+        return host;
+    }
+
+    void prepare() {
+        CUDA_CHECK(cudaSetDevice(dev));
+        if (owned) {
+            CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            CUDA_CHECK(cudaEventCreate(&evh));
+            CUDA_CHECK(cudaEventCreate(&ev0));
+            CUDA_CHECK(cudaEventCreate(&ev1));
+        } else {
+            st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
+            evh = C.evh;
+            ev0 = C.ev0;
+            ev1 = C.ev1;
+        }
+        W = pick_w(g.n);
+        npad = 32 * W;
+        entry = dense_record_bytes(W);
+        out.engine = 1;
+        out.degree_bytes = 2;
+        out.n_padded = npad;
+
+        CUDA_CHECK(cudaEventRecord(evh, st));
+        const DeviceGraph* dgp;
+        if (owned) {
+            std::lock_guard<std::mutex> lk(C.solve_mu);  // (the lazily built device graph)
+            dgp = &device_graph(g, dev, st, &out);
+        } else {
+            dgp = &device_graph(g, dev, st, &out);
+        }
+        const DeviceGraph& dg = *dgp;
+
+        // worker grid: one warp per worker
+        block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
+        block = 32 * block_warps;
+        // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
+        smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + (size_t)block_warps * W * 32 * 4;
+        int per_sm = 1;
+        switch (W) {
+            case 4: per_sm = occupancy<4>(block, smem, s.instrument); break;
+            case 8: per_sm = occupancy<8>(block, smem, s.instrument); break;
+            case 16: per_sm = occupancy<16>(block, smem, s.instrument); break;
+            default: per_sm = occupancy<32>(block, smem, s.instrument); break;
+        }
+        if (per_sm < 1) throw std::runtime_error("CUDA error: dense kernel cannot be resident");
+        workers = s.workers;
+        if (s.strategy == 1) workers = 1;
+        if (workers == 0) workers = (uint32_t)C.sms * per_sm * block_warps;
+        grid = (workers + block_warps - 1) / block_warps;
+        out.grid = grid;
+        out.block = block;
+
+        // memory: stacks, worklist ring, control, cover slots, stats
+        bound = std::max<uint32_t>(s.stack_bound, 1) + 1;
+        cap = std::max<uint64_t>(std::max<uint64_t>(s.capacity, s.num_seeds), 1);
+        if (cap > (1ull << 30)) throw std::invalid_argument("worklist capacity too large");
+        ring = 2;
+        while (ring < cap) ring <<= 1;
+        const size_t stack_bytes = (size_t)workers * bound * entry;
+        wl_bytes = (size_t)ring * entry;
+        seq_bytes = ring * 8;
+        stacks = (unsigned char*)dalloc(C.stacks, stack_bytes);
+        wl = (unsigned char*)dalloc(C.wl, wl_bytes);
+        seq = (unsigned long long*)dalloc(C.seq, seq_bytes);
+        const size_t slots_bytes = (((size_t)workers * W * 4) + 255) / 256 * 256;
+        misc_bytes = sizeof(Ctl) + slots_bytes + (size_t)workers * sizeof(WStats);
+        misc = (unsigned char*)dalloc(C.misc, misc_bytes);
+        ctl = reinterpret_cast<Ctl*>(misc);
+        cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
+        stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
+
+        // initial worklist content: the root (init_root, search_node.cpp:7-14), the seeds, or
+        // nothing (a shard with an empty share)
+        nseeds = s.num_seeds ? s.num_seeds : (s.no_root ? 0 : 1);
+        std::vector<unsigned char> recs(nseeds * entry);
+        if (s.num_seeds) {
+            for (uint64_t i = 0; i < nseeds; ++i) {
+                const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
+                pack_record(W, g.n, r[0], r[1], r + 2, recs.data() + i * entry);
+            }
+        } else if (nseeds) {
+            std::vector<uint32_t> deg(g.n);
+            for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
+            pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs.data());
+        }
+        std::memset(&hc, 0, sizeof(hc));
+        hc.best = s.best;
+        hc.head = 0;
+        hc.tail = nseeds;
+        hc.work = (nseeds << 32) | nseeds;
+        hc.best_owner = ~0ull;
+        CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+        if (nseeds)
+            CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+        init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
+        CUDA_CHECK(cudaGetLastError());
+        out.launches += 2;  // init_seq_kernel + dense_kernel
+        CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
+        out.h2d_bytes += sizeof(hc) + recs.size();
+        if (owned) CUDA_CHECK(cudaStreamSynchronize(st));  // (peers may map it before launch)
+
+        a = DenseArgs{};
+        a.at4 = dg.at4;
+        a.n = g.n;
+        a.npad = npad;
+        a.m = (uint32_t)g.m;
+        a.pvc = s.pvc ? 1 : 0;
+        a.k = s.k;
+        a.capacity = (uint32_t)cap;
+        a.ring_mask = (uint32_t)(ring - 1);
+        a.threshold = (uint32_t)std::min<uint64_t>(s.threshold, cap);
+        a.workers = workers;
+        a.stack_bound = bound;
+        a.entry_bytes = entry;
+        a.stacks = stacks;
+        a.wl = wl;
+        a.seq = seq;
+        a.ctl = ctl;
+        a.cover_slots = cover_slots;
+        a.stats = stats;
+        a.node_budget = s.node_budget;
+        a.timeout_ns = s.timeout_s >= 0 ? (unsigned long long)(s.timeout_s * 1e9) : 0ull;
+        if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
+        a.flush_every = 64;
+        if (s.node_budget)
+            a.flush_every = std::max<uint64_t>(1, std::min<uint64_t>(64, s.node_budget / (4ull * workers)));
+        // idle back-off: exponential from 32 ns, capped at backoff_us (at most 2 us on the device —
+        // a polling warp costs one L2 read, an over-sleeping one leaves queued work unclaimed)
+        a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
+        a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
+        a.donate_oldest = s.donate_oldest ? 1 : 0;
+        a.compact = s.engine == 3 ? 0 : 1;
+        a.stackonly = s.strategy == 2 ? 1 : 0;
+        a.depth = s.depth;
+        a.mailbox = s.mailbox;
+        a.peers = nullptr;
+        a.world = 1;
+        a.rank = 0;
+    }
+
+    // Multi-shard: every shard's exchange memory (this one's included, at `rank`).
+    void link(uint32_t world, uint32_t rank, const std::vector<PeerRef>& refs, uint32_t active) {
+        CUDA_CHECK(cudaSetDevice(dev));
+        CUDA_CHECK(cudaMalloc(&peers_dev, world * sizeof(PeerRef)));
+        CUDA_CHECK(cudaMemcpy(peers_dev, refs.data(), world * sizeof(PeerRef), cudaMemcpyHostToDevice));
+        a.peers = peers_dev;
+        a.world = world;
+        a.rank = rank;
+        if (rank == 0)  // shard 0 holds the shard-activity count
+            CUDA_CHECK(cudaMemcpy(&ctl->gactive, &active, 4, cudaMemcpyHostToDevice));
+    }
+
+    void launch() {
+        CUDA_CHECK(cudaSetDevice(dev));
+        CUDA_CHECK(cudaEventRecord(ev0, st));
+        const bool I = s.instrument;
+        switch (W) {
+            case 4: I ? launch_dense<4, true>(a, grid, block, smem, st) : launch_dense<4, false>(a, grid, block, smem, st); break;
+            case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
+            case 16: I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st); break;
+            default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
+        }
+        CUDA_CHECK(cudaEventRecord(ev1, st));
+    }
+
+    // Kernel done → control block + per-worker stats into pinned memory with one stream sync;
+    // device_ms from the kernel's events, h2d_ms from the upload's.
+    void finish() {
+        CUDA_CHECK(cudaSetDevice(dev));
+        const size_t sb = (size_t)workers * sizeof(WStats);
+        constexpr size_t kStatsAt = (sizeof(Ctl) + 255) / 256 * 256;
+        unsigned char* h = static_cast<unsigned char*>(halloc(kStatsAt + sb));
+        CUDA_CHECK(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaMemcpyAsync(h + kStatsAt, stats, sb, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev0, ev1));
+        out.device_ms = ms;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, evh, ev0));
+        out.h2d_ms = ms;
+        std::memcpy(&hc, h, sizeof(Ctl));
+        out.d2h_bytes += sizeof(Ctl) + sb;
+        const WStats* hs = reinterpret_cast<const WStats*>(h + kStatsAt);
+        out.status = hc.status;
+        out.wl_added = hc.tail;  // every enqueue ticket is one added node (root/seeds included)
+        out.wl_current = (uint32_t)hc.work;
+        out.wl_removed = hc.tail - out.wl_current;
+        out.wl_max_size = nseeds;
+        aggregate(hs, workers, out);
+        if (s.strategy == 2) out.wl_added = out.wl_removed = out.wl_current = out.wl_max_size = 0;
+        if (hc.best_owner != ~0ull) {
+            const uint32_t owner = (uint32_t)(hc.best_owner & 0xFFFFFFFFu);
+            out.found = true;
+            out.found_size = (uint32_t)(hc.best_owner >> 32);
+            std::vector<uint32_t> bits(W);
+            CUDA_CHECK(cudaMemcpy(bits.data(), cover_slots + (size_t)owner * W, W * 4, cudaMemcpyDeviceToHost));
+            out.d2h_bytes += W * 4;
+            out.cover.clear();
+            for (uint32_t v = 0; v < g.n; ++v)
+                if ((bits[v >> 5] >> (v & 31)) & 1u) out.cover.push_back(v);
+        }
+    }
+};
+
+namespace {
+void check_dense_device(const Graph& g, const SolveSpec& s) {
+    if (g.n > 1024)
+        throw std::invalid_argument("graph has " + std::to_string(g.n) +
+                                    " vertices; the dense engine handles n <= 1024");
+    int ndev = device_count();
+    if (ndev == 0) throw std::runtime_error("CUDA error: no CUDA device visible");
+    if (s.device < 0 || s.device >= ndev) throw std::invalid_argument("device ordinal out of range");
+}
+}  // namespace
+
+void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
+    if (s.engine == 2 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
+    check_dense_device(g, s);
+    CUDA_CHECK(cudaSetDevice(s.device));
+    DeviceCtx& C = ctx_for(s.device);
+    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
+    DenseRun r(g, s, false);
+    r.out = std::move(out);
+    r.prepare();
+    r.launch();
+    r.finish();
+    out = std::move(r.out);
+}
+
+// ------------------------------------------------------------------ multi-shard sessions
+
+struct Session {
+    std::unique_ptr<DenseRun> run;
+};
+
+Session* session_open(const Graph& g, const SolveSpec& s) {
+    if (s.engine == 2 || g.n > 1024)
+        throw std::invalid_argument("multi-shard sessions need the dense engine (n <= 1024)");
+    check_dense_device(g, s);
+    if (s.strategy != 0) throw std::invalid_argument("multi-shard sessions run the hybrid strategies");
+    auto ses = std::make_unique<Session>();
+    ses->run = std::make_unique<DenseRun>(g, s, true);
+    ses->run->prepare();
+    return ses.release();
+}
+
+void session_close(Session* ses) { delete ses; }
+
+size_t session_handle_bytes() { return 3 * sizeof(cudaIpcMemHandle_t); }
+
+void session_export(const Session* ses, void* handle) {
+    const DenseRun& r = *ses->run;
+    CUDA_CHECK(cudaSetDevice(r.dev));
+    cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(handle);
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[0], r.misc));
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[1], r.wl));
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[2], r.seq));
+}
+
+static uint32_t shard_active(const Session* ses) { return ses->run->nseeds ? 1u : 0u; }
+
+void session_link_ipc(Session* ses, uint32_t world, uint32_t rank, const void* handles,
+                      const uint64_t* seeds_per_shard) {
+    DenseRun& r = *ses->run;
+    if (world < 1 || rank >= world) throw std::invalid_argument("bad shard rank / world");
+    CUDA_CHECK(cudaSetDevice(r.dev));
+    const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+    std::vector<PeerRef> refs(world);
+    uint32_t active = 0;
+    for (uint32_t p = 0; p < world; ++p) {
+        active += seeds_per_shard[p] ? 1u : 0u;
+        if (p == rank) {
+            refs[p] = PeerRef{r.ctl, r.wl, r.seq};
+            continue;
+        }
+        void* ptr[3];
+        for (int t = 0; t < 3; ++t) {
+            CUDA_CHECK(cudaIpcOpenMemHandle(&ptr[t], h[3 * p + t], cudaIpcMemLazyEnablePeerAccess));
+            r.ipc_opened.push_back(ptr[t]);
+        }
+        refs[p] = PeerRef{static_cast<Ctl*>(ptr[0]), static_cast<unsigned char*>(ptr[1]),
+                          static_cast<unsigned long long*>(ptr[2])};
+    }
+    r.link(world, rank, refs, active);
+}
+
+void session_link_local(Session* const* shards, uint32_t world) {
+    std::vector<PeerRef> refs(world);
+    uint32_t active = 0;
+    for (uint32_t p = 0; p < world; ++p) {
+        const DenseRun& r = *shards[p]->run;
+        refs[p] = PeerRef{r.ctl, r.wl, r.seq};
+        active += shard_active(shards[p]);
+    }
+    for (uint32_t p = 0; p < world; ++p) {
+        DenseRun& r = *shards[p]->run;
+        for (uint32_t q = 0; q < world; ++q) {  // shards on different devices: peer access
+            const int dq = shards[q]->run->dev;
+            if (dq == r.dev) continue;
+            CUDA_CHECK(cudaSetDevice(r.dev));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(dq, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_CHECK(e);
+            cudaGetLastError();
+        }
+        r.link(world, p, refs, active);
     }
 }
 
+void session_launch(Session* ses) { ses->run->launch(); }
+
+uint32_t full_device_workers(const Graph& g, int dev) {
+    SolveSpec s;
+    s.device = dev;
+    check_dense_device(g, s);
+    CUDA_CHECK(cudaSetDevice(dev));
+    DeviceCtx& C = ctx_for(dev);
+    const uint32_t W = pick_w(g.n), npad = 32 * W, block = 256;
+    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + 8 * (size_t)W * 32 * 4;
+    int per_sm = 1;
+    switch (W) {
+        case 4: per_sm = occupancy<4>(block, smem, false); break;
+        case 8: per_sm = occupancy<8>(block, smem, false); break;
+        case 16: per_sm = occupancy<16>(block, smem, false); break;
+        default: per_sm = occupancy<32>(block, smem, false); break;
+    }
+    return (uint32_t)C.sms * per_sm * 8;
+}
+
+void session_wait(Session* ses, SolveOut& out) {
+    ses->run->finish();
+    out = std::move(ses->run->out);
+}
+
 // ------------------------------------------------------------------ sparse engine host side
+
 
 static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     const int dev = s.device;

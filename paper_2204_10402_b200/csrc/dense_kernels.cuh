@@ -48,7 +48,10 @@ struct Ctl {
     uint32_t pad2[24];
     // line 1: ring tickets (per-slot sequence numbers publish / free each slot)
     unsigned long long head, tail;
-    uint32_t pad3[28];
+    // shard 0 only (multi-shard solves): number of shards whose `pending` is non-zero; the
+    // whole solve is done when it reaches zero
+    uint32_t gactive;
+    uint32_t pad3[27];
     // line 2: results
     unsigned long long nodes_total, best_owner;
     int32_t status;
@@ -56,9 +59,17 @@ struct Ctl {
 };
 static_assert(sizeof(Ctl) == 384, "Ctl layout");
 
+// A peer shard's exchange memory (another GPU over NVLink P2P / CUDA IPC, or another shard on
+// this device): its control block, ring slots and slot sequence numbers.
+struct PeerRef {
+    Ctl* ctl;
+    unsigned char* wl;
+    unsigned long long* seq;
+};
+
 struct WStats {
     unsigned long long nodes, rounds, maxdeg, children, rm1, rm2, rmh, high_water, donated,
-        active, max_queue, dooms;
+        active, max_queue, dooms, peer;
     unsigned long long phase[10];
 };
 
@@ -93,6 +104,10 @@ struct DenseArgs {
     uint32_t depth;           // StackOnly sub-tree depth (2^depth sub-trees)
     volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out,
                                  // [3] found out
+    // multi-shard solves (world > 1): every shard's exchange memory, this shard's index
+    const PeerRef* peers;
+    uint32_t world, rank;
+    int no_root;                 // this shard starts with an empty worklist
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -116,6 +131,25 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 }
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// system scope: ring publications and control words shared with other GPUs
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -171,7 +205,7 @@ __device__ __noinline__ void poll_mailbox(volatile uint32_t* mb, int pvc, Ctl* c
 template <class T>
 struct CountersT {
     T nodes = 0, rounds = 0, maxdeg = 0, children = 0, rm1 = 0, rm2 = 0, rmh = 0, donated = 0,
-      dooms = 0;
+      dooms = 0, peer = 0;
     T high_water = 0, max_queue = 0;  // maxima
     unsigned long long phase[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
@@ -189,10 +223,11 @@ __device__ __forceinline__ void fold_stats(WStats* o, Counters32& st) {
     o->rmh += st.rmh;
     o->donated += st.donated;
     o->dooms += st.dooms;
+    o->peer += st.peer;
 }
 __device__ __forceinline__ void reset_deltas(Counters32& st) {
     st.nodes = st.rounds = st.maxdeg = st.children = st.rm1 = st.rm2 = st.rmh = st.donated =
-        st.dooms = 0;
+        st.dooms = st.peer = 0;
 }
 
 // ------------------------------------------------------------------ one search node per warp
@@ -893,6 +928,31 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
     return true;
 }
 
+// try_add on a PEER shard's worklist (system-scope atomics over NVLink / IPC). Keeps the
+// shard-activity count exact: whoever moves a shard's `pending` 0 -> 1 adds one to gactive,
+// whoever moves it 1 -> 0 subtracts one.
+__device__ __forceinline__ bool q_reserve_peer(const DenseArgs& a, const PeerRef& pr,
+                                               unsigned long long& pos_out) {
+    uint32_t* const gactive = &a.peers[0].ctl->gactive;
+    const unsigned long long old = atomicAdd_system(&pr.ctl->work, ONE_PENDING | 1ull);
+    if ((old >> 32) == 0) atomicAdd_system(gactive, 1u);
+    if ((uint32_t)old >= a.capacity) {
+        const unsigned long long o2 = atomicAdd_system(&pr.ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
+        if ((o2 >> 32) == 1) atomicSub_system(gactive, 1u);
+        return false;
+    }
+    pos_out = atomicAdd_system(&pr.ctl->tail, 1ull);
+    return true;
+}
+
+// Cancel this shard and every peer (a found PVC cover, a timeout or a node budget ends the whole
+// multi-shard solve).
+__device__ __noinline__ void cancel_all(const DenseArgs& a) {
+    atomicExch(&a.ctl->cancel, 1u);
+    for (uint32_t p = 0; p < a.world; ++p)
+        if (p != a.rank) atomicExch_system(&a.peers[p].ctl->cancel, 1u);
+}
+
 // ------------------------------------------------------------------ the traversal kernel
 
 // Copies one node record (either layout) through L2: `vec16` 16-byte vectors spread over the
@@ -957,6 +1017,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     bool poll = false;
     uint4 h = make_uint4(0, 0, 0, 0);
     unsigned long long hw = 0;
+    // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
+    const bool multi = a.world > 1;
+    uint32_t starve = a.world, hp = a.world, probe = 0;
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto settle = [&](auto& n) -> int {
@@ -968,6 +1031,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 B = bound_of(0, 0, best);
             }
             qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+            if (multi) starve = __shfl_sync(FULL, hp, 0);
         }
         const bool prune = n.doom || prune_at(B, n.cc, n.edges);
         st.dooms += n.doom;
@@ -986,7 +1050,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 __syncwarp();
                 if (lane == 0) {
                     atomicMin(&ctl->best_owner, ((unsigned long long)n.cc << 32) | worker);
-                    if (a.pvc) atomicExch(&ctl->cancel, 1u);
+                    if (a.pvc) cancel_all(a);
+                    else
+                        for (uint32_t p = 0; p < a.world; ++p)  // the bound reaches every shard
+                            if (p != a.rank) atomicMin_system(&a.peers[p].ctl->best, n.cc);
                     if (a.mailbox) {
                         a.mailbox[2] = n.cc;
                         if (a.pvc) a.mailbox[3] = 1;
@@ -1060,6 +1127,28 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 ++st.donated;
             }
         }
+        bool remote = false;
+        if (multi && !publish && starve < a.world && sp > 0 && !a.seq_mode) {
+            // Work donation between shards: a peer below its threshold gets this worker's
+            // oldest stacked node, written straight into its ring slot over NVLink / IPC.
+            const PeerRef& pr = a.peers[starve];
+            int ok = 0;
+            if (lane == 0) ok = q_reserve_peer(a, pr, pos);
+            if (__shfl_sync(FULL, ok, 0)) {
+                pos = __shfl_sync(FULL, pos, 0);
+                publish = pr.seq + (pos & a.ring_mask);
+                if (lane == 0)
+                    while (ld_acquire_sys_u64(publish) != pos) __nanosleep(64);
+                __syncwarp();
+                copy_record_raw(slot_at(0), pr.wl + (pos & a.ring_mask) * a.entry_bytes, vec16, lane);
+                base = base + 1 == a.stack_bound ? 0 : base + 1;
+                --sp;
+                ++st.donated;
+                ++st.peer;
+                remote = true;
+            }
+            starve = a.world;  // (re-armed by the next poll)
+        }
         if (build && (!dead || a.seq_mode)) {
             if (!child) {
                 child = slot_at(sp);
@@ -1075,7 +1164,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         }
         if (publish) {
             __syncwarp();  // (the release by lane 0 is cumulative over the warp's stores)
-            if (lane == 0) st_release_u64(publish, pos + 1);
+            if (lane == 0) {
+                if (remote) st_release_sys_u64(publish, pos + 1);
+                else st_release_u64(publish, pos + 1);
+            }
         }
         if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
         if (right) return ACT_POP;  // replay continues with the remove-N(v) child just stacked
@@ -1112,7 +1204,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 // GlobalWorklist::remove_or_done (worklist.cpp:21-48): take a ticket, then wait
                 // for that slot's publication, for termination (pending == 0) or a cancel.
                 if (!idle) {
-                    if (lane == 0) atomicAdd(&ctl->work, ~ONE_PENDING + 1ull);  // pending - 1
+                    if (lane == 0) {
+                        const unsigned long long o = atomicAdd(&ctl->work, ~ONE_PENDING + 1ull);
+                        if (multi && (o >> 32) == 1) {  // this shard went idle
+                            __threadfence_system();
+                            atomicSub_system(&a.peers[0].ctl->gactive, 1u);
+                        }
+                    }
                     idle = true;
                 }
                 if (lane == 0) pos = atomicAdd(&ctl->head, 1ull);
@@ -1124,11 +1222,18 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 for (uint32_t spin = 0;; ++spin) {
                     int o = 0;
                     if (lane == 0) {
-                        if (ld_acquire_u64(release) == pos + 1) o = 1;
+                        if ((multi ? ld_acquire_sys_u64(release) : ld_acquire_u64(release)) == pos + 1) o = 1;
                         else if ((spin & 7) == 7) {
                             if (ld_volatile_v4(ctl).y) o = 2;
-                            else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0) o = 2;
+                            else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0 &&
+                                     (!multi || ld_acquire_sys_u32(&a.peers[0].ctl->gactive) == 0))
+                                o = 2;  // every shard idle: nothing can create work again
                             else if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+                            else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) {
+                                atomicCAS(&ctl->status, 0, 1);
+                                cancel_all(a);
+                                o = 2;
+                            }
                         }
                     }
                     outcome = __shfl_sync(FULL, o, 0);
@@ -1140,7 +1245,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                     if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
                     break;
                 }
-                (void)ld_acquire_u64(release);  // every lane acquires the publication
+                // every lane acquires the publication
+                (void)(multi ? ld_acquire_sys_u64(release) : ld_acquire_u64(release));
                 src = a.wl + (pos & a.ring_mask) * a.entry_bytes;
                 idle = false;
             }
@@ -1171,6 +1277,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         if (poll && lane == 0) {
             h = ld_volatile_v4(ctl);
             hw = ld_relaxed_u64(&ctl->work);
+            if (multi) {  // one peer per poll, round robin: is it below its donation threshold?
+                const uint32_t p = (a.rank + 1 + probe++ % (a.world - 1)) % a.world;
+                hp = (uint32_t)ld_relaxed_sys_u64(&a.peers[p].ctl->work) < a.threshold ? p : a.world;
+            }
         }
 
         // visit_and_check_limits (scheduler.cpp:63-74), batched per flush_every visits
@@ -1184,7 +1294,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) stop = 1;
                 if (stop) {
                     atomicCAS(&ctl->status, 0, stop);
-                    atomicExch(&ctl->cancel, 1u);
+                    cancel_all(a);
                 }
                 if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
                 fold_stats(my_stats, st);

@@ -32,6 +32,7 @@ struct SolveSpec {
     uint64_t num_seeds = 0;
     volatile uint32_t* mailbox = nullptr;
     void* stream = nullptr;     // caller's cudaStream_t (null: the library's stream)
+    bool no_root = false;       // multi-shard: no seeds means an empty worklist, not the root
 };
 
 struct SolveOut {
@@ -45,6 +46,7 @@ struct SolveOut {
     uint64_t rm1 = 0, rm2 = 0, rmh = 0, dooms = 0;
     uint64_t phase[10] = {0};
     uint64_t active_cycles = 0;
+    uint64_t donated_peer = 0;
     double device_ms = 0, h2d_ms = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;
     uint32_t degree_bytes = 2, n_padded = 0;
@@ -68,6 +70,24 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
 
 // Throws std::runtime_error (CUDA failures) / std::invalid_argument (bad configuration).
 void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out);
+
+// Multi-shard solves (one shard per GPU, or several on one device): each shard is a dense-engine
+// run with its own worklist; linked shards donate work into each other's rings and share the
+// MVC bound, the PVC found flag and termination through peer memory (NVLink P2P / CUDA IPC).
+struct Session;
+Session* session_open(const Graph& g, const SolveSpec& s);  // prepare: buffers + seeds
+size_t session_handle_bytes();
+void session_export(const Session* ses, void* handle);     // CUDA IPC handles of its exchange memory
+// link to every shard's exported handles (this process owns shard `rank`)
+void session_link_ipc(Session* ses, uint32_t world, uint32_t rank, const void* handles,
+                      const uint64_t* seeds_per_shard);
+// link shards living in this process (same or peer-accessible devices)
+void session_link_local(Session* const* shards, uint32_t world);
+void session_launch(Session* ses);                 // asynchronous
+void session_wait(Session* ses, SolveOut& out);    // blocks, assembles the result
+void session_close(Session* ses);
+// Workers (warps) of a full-device dense solve of g: shards sharing a device split these.
+uint32_t full_device_workers(const Graph& g, int dev);
 int device_count();
 uint32_t* mailbox_alloc(uint32_t n_words);
 void mailbox_free(uint32_t* p);

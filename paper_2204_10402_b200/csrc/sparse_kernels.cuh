@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         o.dooms = st.dooms;
         o.high_water = st.high_water;
         o.donated = st.donated;
+        o.peer = 0;
         o.active = clock64() - c_start;
         o.max_queue = st.max_queue;
 #pragma unroll

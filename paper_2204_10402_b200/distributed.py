@@ -142,13 +142,21 @@ def _empty_result(graph, pvc):
 
 def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_per_rank=1024,
                       device=0, stream=None, period=0.002, solver=None, expander=None,
-                      mailbox=None, **solve_kw):
+                      mailbox=None, exchange="peer", shard_factory=None, **solve_kw):
     """One rank's part of a multi-GPU solve; every rank of ``exchange_group`` (a CPU/gloo
     process group; default: the world group) must call it. Returns the combined result
-    (identical on every rank): size/feasible/cover, per-rank node counts and timings."""
+    (identical on every rank): size/feasible/cover, per-rank node counts and timings.
+
+    ``exchange="peer"``: the ranks' device worklists are linked through CUDA IPC / NVLink P2P
+    (``shards.Shard``) — work donation between GPUs, peer-atomic bound, shared termination; the
+    CPU group only carries the IPC handles once. ``exchange="host"``: static shares, bound and
+    found flag through the host monitor below."""
     import torch.distributed as dist
     if mode == "pvc" and k < 1:
         raise ValueError("pvc requires k >= 1")
+    if exchange == "peer" and solver is None:
+        return _solve_peer(graph, mode, k, exchange_group, frontier_per_rank, device,
+                           expander or expand_frontier, shard_factory, solve_kw)
     pvc = mode == "pvc"
     rank = dist.get_rank(exchange_group)
     world = dist.get_world_size(exchange_group)
@@ -216,3 +224,41 @@ def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_p
                 worker_nodes=[w for r in allr for w in r["worker_nodes"]],
                 kernel_launches=fr["kernel_launches"] + mine["launches"],
                 exchange_rounds=mon.rounds, greedy_size=fr["greedy_size"])
+
+
+def _solve_peer(graph, mode, k, group, frontier_per_rank, device, expander, shard_factory,
+                solve_kw):
+    """solve_distributed with device-linked worklists (see shards.py)."""
+    import torch.distributed as dist
+    from .shards import Shard, combine
+    Shard = shard_factory or Shard
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    t0 = time.perf_counter()
+    fr = expander(graph, mode, k, frontier_per_rank * world, device=device)
+    fr["frontier_size"] = int(len(fr["seeds"]))
+    share = fr["seeds"][rank::world]
+    parts = []
+    if not (mode == "pvc" and fr["found"]) and len(fr["seeds"]):
+        extra = {} if mode == "pvc" else {"initial_best": fr["best"]}
+        shard = Shard(graph, mode, k, seeds=share if len(share) else None, device=device,
+                      **extra, **solve_kw)
+        try:
+            handles = [None] * world
+            dist.all_gather_object(handles, shard.export(), group=group)
+            units = [None] * world
+            dist.all_gather_object(units, shard.work_units, group=group)
+            shard.link_ipc(world, rank, handles, units)
+            dist.barrier(group=group)  # every shard linked (shard 0's count set) before launch
+            shard.launch()
+            mine = shard.wait()
+            dist.barrier(group=group)  # no peer unmaps while another kernel may still write
+        finally:
+            shard.close()
+        keep = ("size", "feasible", "cover", "cover_from_search", "status", "worker_nodes",
+                "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches")
+        parts = [None] * world
+        dist.all_gather_object(parts, {x: mine[x] for x in keep}, group=group)
+    out = combine(graph, mode, fr, parts, (time.perf_counter() - t0) * 1e3)
+    out["exchange"] = "peer"
+    return out

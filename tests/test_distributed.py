@@ -171,3 +171,78 @@ def test_frontier_decides_without_search_on_three_ranks(mode):
         assert log["calls"] == 0
         assert r["feasible"] and r["size"] == 3 and r["cover"] == [0, 2, 4]
         assert r["nodes_total"] == 7
+
+
+# ---- exchange="peer": the IPC-handle rendezvous and the combination, with a stand-in shard --
+
+class FakeShard:
+    """Records what solve_distributed asks of a shards.Shard (no device)."""
+    log = None
+
+    def __init__(self, graph, mode, k, *, seeds=None, device=0, **kw):
+        self.seeds = seeds
+        self.kw = kw
+        self.rank = None
+        FakeShard.log["opened"] = dict(n=0 if seeds is None else len(seeds), kw=sorted(kw))
+
+    @property
+    def work_units(self):
+        return 0 if self.seeds is None else len(self.seeds)
+
+    def export(self):
+        return bytes([dist.get_rank()]) * 8
+
+    def link_ipc(self, world, rank, handles, units):
+        FakeShard.log["link"] = dict(world=world, rank=rank, handles=handles, units=list(units))
+
+    def launch(self):
+        FakeShard.log["launched"] = True
+
+    def wait(self):
+        n = self.work_units
+        return dict(size=0, feasible=False, cover=[], cover_from_search=False, status="complete",
+                    worker_nodes=[n], nodes_total=10 * n, device_ms=1.0, donated=n,
+                    donated_peer=1, kernel_launches=2)
+
+    def close(self):
+        FakeShard.log["closed"] = True
+
+
+def worker_peer(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_10402_b200.distributed import solve_distributed
+    FakeShard.log = {}
+    r = solve_distributed(FakeGraph(), "pvc", 4, frontier_per_rank=2, expander=fake_expander,
+                          shard_factory=FakeShard, exchange="peer", timeout_s=5)
+    out.put((rank, r, FakeShard.log))
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_rendezvous_on_three_ranks():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=worker_peer, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in range(world):
+        rank, r, log = q.get(timeout=120)
+        got[rank] = (r, log)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = 2 * world + 3  # fake_expander: target + 3 seed records, dealt i % world
+    shares = [len(range(rk, total, world)) for rk in range(world)]
+    for rank, (r, log) in got.items():
+        assert log["opened"]["n"] == shares[rank] and log["opened"]["kw"] == ["timeout_s"]
+        assert log["link"]["world"] == world and log["link"]["rank"] == rank
+        assert log["link"]["handles"] == [bytes([q]) * 8 for q in range(world)]  # rank order
+        assert log["link"]["units"] == shares
+        assert log["launched"] and log["closed"]
+        assert r["exchange"] == "peer" and not r["feasible"] and r["status"] == "complete"
+        assert r["nodes_total"] == 100 + 10 * total
+        assert r["rank_nodes"] == [10 * n for n in shares]
+        assert r["rank_donated_peer"] == [1] * world

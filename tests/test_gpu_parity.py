@@ -325,3 +325,50 @@ def test_stackonly_load_imbalance_vs_hybrid(config_golden):
     hy = vc.solve_mvc(g, strategy="hybrid", workers=256)
     assert so["size"] == hy["size"] == config_golden["c3"]["mvc"]
     assert max(hy["load_ratios"]) < max(so["load_ratios"])
+
+
+# ---- multi-shard solves: device worklists linked through peer memory (shards.py) ----------
+
+@pytest.mark.parametrize("skew", [False, True])
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_sharded_pvc_pair_exact(config_golden, name, skew):
+    """Two shards on one device: the no-instance tree is visited exactly once across shards and
+    the frontier (node count = the reference's), the yes-instance yields a verified cover."""
+    from paper_2204_10402_b200.shards import solve_sharded
+    g = load_config(name)
+    gold = config_golden[name]
+    no = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=(0, 0), skew=skew, timeout_s=60)
+    assert no["status"] == "complete" and not no["feasible"]
+    assert no["nodes_total"] == gold["pvc_no_nodes"], (no["nodes_total"], no["rank_nodes"])
+    if skew and no["rank_nodes"]:  # shard 1 starts empty: all it visits was donated to it
+        assert no["rank_nodes"][1] > 0, no["rank_nodes"]
+    yes = solve_sharded(g, "pvc", gold["mvc"], devices=(0, 0), skew=skew, timeout_s=60)
+    assert yes["feasible"] and len(yes["cover"]) <= gold["mvc"]
+    assert vc.verify_cover(g, yes["cover"])
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_sharded_mvc_optimum(config_golden, name):
+    from paper_2204_10402_b200.shards import solve_sharded
+    g = load_config(name)
+    r = solve_sharded(g, "mvc", devices=(0, 0, 0), skew=True, timeout_s=60)
+    assert r["status"] == "complete" and r["size"] == config_golden[name]["mvc"]
+    assert vc.verify_cover(g, r["cover"])
+
+
+def test_sharded_c5_no_instance(config_golden):
+    from paper_2204_10402_b200.shards import solve_sharded
+    gold = config_golden["c5"]
+    g = load_config("c5")
+    r = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=(0, 0), frontier_per_shard=256,
+                      timeout_s=120)
+    assert r["status"] == "complete" and not r["feasible"]
+    assert r["nodes_total"] == gold["pvc_no_nodes"]
+    assert min(r["rank_nodes"]) > 0
+
+
+def test_sharded_timeout_cancels_every_shard():
+    from paper_2204_10402_b200.shards import solve_sharded
+    g = load_config("c5")
+    r = solve_sharded(g, "pvc", 482, devices=(0, 0), timeout_s=0.002)
+    assert r["status"] == "timeout"
