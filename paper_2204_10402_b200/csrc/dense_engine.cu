@@ -189,9 +189,12 @@ void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint
         }
 }
 
+// Instantiations: (instrumented | plain) single-shard kernels, plus the plain multi-shard one.
 template <int W, bool INSTR>
 void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s) {
-    auto k = dense_kernel<W, INSTR>;
+    if (INSTR && a.world > 1)
+        throw std::invalid_argument("instrumented runs are single-shard");
+    auto k = a.world > 1 ? dense_kernel<W, false, true> : dense_kernel<W, INSTR, false>;
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, block, smem, s>>>(a);
     CUDA_CHECK(cudaGetLastError());
@@ -200,7 +203,7 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
 template <int W>
 int occupancy(uint32_t block, size_t smem, bool instr) {
     int nb = 0;
-    auto k = instr ? dense_kernel<W, true> : dense_kernel<W, false>;
+    auto k = instr ? dense_kernel<W, true, false> : dense_kernel<W, false, false>;
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)block, smem));
     return nb;

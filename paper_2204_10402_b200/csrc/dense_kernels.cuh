@@ -928,32 +928,14 @@ __device__ __forceinline__ bool q_reserve(const DenseArgs& a, unsigned long long
     return true;
 }
 
-// try_add on a PEER shard's worklist (system-scope atomics over NVLink / IPC). Keeps the
-// shard-activity count exact: whoever moves a shard's `pending` 0 -> 1 adds one to gactive,
-// whoever moves it 1 -> 0 subtracts one.
-__device__ __forceinline__ bool q_reserve_peer(const DenseArgs& a, const PeerRef& pr,
-                                               unsigned long long& pos_out) {
-    uint32_t* const gactive = &a.peers[0].ctl->gactive;
-    const unsigned long long old = atomicAdd_system(&pr.ctl->work, ONE_PENDING | 1ull);
-    if ((old >> 32) == 0) atomicAdd_system(gactive, 1u);
-    if ((uint32_t)old >= a.capacity) {
-        const unsigned long long o2 = atomicAdd_system(&pr.ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
-        if ((o2 >> 32) == 1) atomicSub_system(gactive, 1u);
-        return false;
-    }
-    pos_out = atomicAdd_system(&pr.ctl->tail, 1ull);
-    return true;
+// (By value: a reference to the kernel parameters would force them into local memory.)
+__device__ __noinline__ void cancel_all_(Ctl* ctl, const PeerRef* peers, uint32_t world,
+                                         uint32_t rank) {
+    atomicExch(&ctl->cancel, 1u);
+    for (uint32_t p = 0; p < world; ++p)
+        if (p != rank) atomicExch_system(&peers[p].ctl->cancel, 1u);
 }
-
-// Cancel this shard and every peer (a found PVC cover, a timeout or a node budget ends the whole
-// multi-shard solve).
-__device__ __noinline__ void cancel_all(const DenseArgs& a) {
-    atomicExch(&a.ctl->cancel, 1u);
-    for (uint32_t p = 0; p < a.world; ++p)
-        if (p != a.rank) atomicExch_system(&a.peers[p].ctl->cancel, 1u);
-}
-
-// ------------------------------------------------------------------ the traversal kernel
+#define cancel_all(a) cancel_all_((a).ctl, (a).peers, (a).world, (a).rank)
 
 // Copies one node record (either layout) through L2: `vec16` 16-byte vectors spread over the
 // warp's lanes.
@@ -964,9 +946,79 @@ __device__ __forceinline__ void copy_record_raw(const unsigned char* src, unsign
         reinterpret_cast<uint4*>(dst)[t] = __ldcg(reinterpret_cast<const uint4*>(src) + t);
 }
 
+// Work donation between shards (cold): reserve a slot in peer `pr`'s ring, copy the record at
+// `src` into it over NVLink / IPC, publish it with a system-scope release. Warp-collective.
+__device__ __noinline__ bool donate_to_peer(const PeerRef* pr, Ctl* ctl0, uint32_t capacity,
+                                            uint32_t ring_mask, unsigned long long entry_bytes,
+                                            const unsigned char* src, int lane) {
+    uint32_t* const gactive = &ctl0->gactive;
+    unsigned long long pos = 0;
+    int ok = 0;
+    if (lane == 0) {
+        const unsigned long long old = atomicAdd_system(&pr->ctl->work, ONE_PENDING | 1ull);
+        if ((old >> 32) == 0) atomicAdd_system(gactive, 1u);  // the peer's pending 0 -> 1
+        if ((uint32_t)old >= capacity) {
+            const unsigned long long o2 =
+                atomicAdd_system(&pr->ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
+            if ((o2 >> 32) == 1) atomicSub_system(gactive, 1u);  // and back 1 -> 0
+        } else {
+            pos = atomicAdd_system(&pr->ctl->tail, 1ull);
+            ok = 1;
+        }
+    }
+    if (!__shfl_sync(FULL, ok, 0)) return false;
+    pos = __shfl_sync(FULL, pos, 0);
+    unsigned long long* publish = pr->seq + (pos & ring_mask);
+    if (lane == 0)
+        while (ld_acquire_sys_u64(publish) != pos) __nanosleep(64);
+    __syncwarp();
+    copy_record_raw(src, pr->wl + (pos & ring_mask) * entry_bytes, (uint32_t)(entry_bytes / 16), lane);
+    __syncwarp();
+    if (lane == 0) st_release_sys_u64(publish, pos + 1);
+    return true;
+}
+
+// record_cover (scheduler.cpp:84-108) once the warp holds a cover: MVC keeps it if it beats the
+// bound (every shard's bound is lowered), PVC keeps the first and ends the search everywhere.
+// Returns true when the search is over (PVC). Cold: out of the node loop's code.
+__device__ __noinline__ bool record_cover_(Ctl* ctl, uint32_t* cover_slots, volatile uint32_t* mailbox,
+                                           const PeerRef* peers, uint32_t world, uint32_t rank,
+                                           int pvc, uint32_t W, uint32_t worker, uint32_t cc,
+                                           uint32_t wbits, int lane) {
+    uint32_t record = 0;
+    if (lane == 0) {
+        if (pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
+        else record = cc < atomicMin(&ctl->best, cc);
+    }
+    if (__shfl_sync(FULL, record, 0)) {
+        if (lane < (int)W) cover_slots[(unsigned long long)worker * W + lane] = wbits;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            atomicMin(&ctl->best_owner, ((unsigned long long)cc << 32) | worker);
+            if (pvc) {
+                cancel_all_(ctl, peers, world, rank);
+            } else {
+                for (uint32_t p = 0; p < world; ++p)  // the bound reaches every shard
+                    if (p != rank) atomicMin_system(&peers[p].ctl->best, cc);
+            }
+            if (mailbox) {
+                mailbox[2] = cc;
+                if (pvc) mailbox[3] = 1;
+            }
+        }
+    }
+    return pvc != 0;
+}
+#define record_cover(a, worker, cc, wbits, lane)                                                 \
+    record_cover_((a).ctl, (a).cover_slots, (a).mailbox, (a).peers, (a).world, (a).rank, (a).pvc, \
+                  W, worker, cc, wbits, lane)
+
+// ------------------------------------------------------------------ the traversal kernel
+
 enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
 
-template <int W, bool INSTR>
+template <int W, bool INSTR, bool MULTI>
 #ifndef VCG_MINB16
 #define VCG_MINB16 2  // CTAs of 8 warps per SM targeted by the W=16 register allocation
 #endif               // (with the compact layout: 2 → 128 regs, C5 12.5 ms; 3 → 80 + spills, 13.1)
@@ -1018,7 +1070,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     uint4 h = make_uint4(0, 0, 0, 0);
     unsigned long long hw = 0;
     // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
-    const bool multi = a.world > 1;
+    const bool multi = MULTI;  // linked shards (a separate instantiation: the single-shard
+                               // kernel carries none of the peer code)
     uint32_t starve = a.world, hp = a.world, probe = 0;
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
@@ -1038,29 +1091,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         if (prune) return ACT_POP;
         if (n.edges == 0) {
             // record_cover (scheduler.cpp:84-108)
-            uint32_t record = 0;
-            if (lane == 0) {
-                if (a.pvc) record = atomicCAS(&ctl->found, 0u, 1u) == 0u;
-                else record = n.cc < atomicMin(&ctl->best, n.cc);
-            }
-            if (__shfl_sync(FULL, record, 0)) {
-                const uint32_t wbits = n.template cover_word<W>(sb);
-                if (lane < W) a.cover_slots[(unsigned long long)worker * W + lane] = wbits;
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) {
-                    atomicMin(&ctl->best_owner, ((unsigned long long)n.cc << 32) | worker);
-                    if (a.pvc) cancel_all(a);
-                    else
-                        for (uint32_t p = 0; p < a.world; ++p)  // the bound reaches every shard
-                            if (p != a.rank) atomicMin_system(&a.peers[p].ctl->best, n.cc);
-                    if (a.mailbox) {
-                        a.mailbox[2] = n.cc;
-                        if (a.pvc) a.mailbox[3] = 1;
-                    }
-                }
-            }
-            if (a.pvc) return ACT_BREAK;  // the search is ended (solver_seq.cpp:108)
+            const uint32_t wbits = n.template cover_word<W>(sb);
+            if (record_cover(a, worker, n.cc, wbits, lane)) return ACT_BREAK;  // PVC: ended
             best = min(best, n.cc);
             B = bound_of(0, 0, best);
             return ACT_POP;
@@ -1127,25 +1159,15 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 ++st.donated;
             }
         }
-        bool remote = false;
         if (multi && !publish && starve < a.world && sp > 0 && !a.seq_mode) {
             // Work donation between shards: a peer below its threshold gets this worker's
             // oldest stacked node, written straight into its ring slot over NVLink / IPC.
-            const PeerRef& pr = a.peers[starve];
-            int ok = 0;
-            if (lane == 0) ok = q_reserve_peer(a, pr, pos);
-            if (__shfl_sync(FULL, ok, 0)) {
-                pos = __shfl_sync(FULL, pos, 0);
-                publish = pr.seq + (pos & a.ring_mask);
-                if (lane == 0)
-                    while (ld_acquire_sys_u64(publish) != pos) __nanosleep(64);
-                __syncwarp();
-                copy_record_raw(slot_at(0), pr.wl + (pos & a.ring_mask) * a.entry_bytes, vec16, lane);
+            if (donate_to_peer(a.peers + starve, a.peers[0].ctl, a.capacity, a.ring_mask,
+                               a.entry_bytes, slot_at(0), lane)) {
                 base = base + 1 == a.stack_bound ? 0 : base + 1;
                 --sp;
                 ++st.donated;
                 ++st.peer;
-                remote = true;
             }
             starve = a.world;  // (re-armed by the next poll)
         }
@@ -1164,10 +1186,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         }
         if (publish) {
             __syncwarp();  // (the release by lane 0 is cumulative over the warp's stores)
-            if (lane == 0) {
-                if (remote) st_release_sys_u64(publish, pos + 1);
-                else st_release_u64(publish, pos + 1);
-            }
+            if (lane == 0) st_release_u64(publish, pos + 1);
         }
         if (INSTR) st.phase[publish ? PH_WL_ADD : PH_BRANCH_NBRS] += clock64() - tb;
         if (right) return ACT_POP;  // replay continues with the remove-N(v) child just stacked

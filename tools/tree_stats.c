@@ -117,6 +117,8 @@ static int reduce(node_t* x, uint32_t k) {
 }
 
 static node_t stack_[4096];
+static uint32_t depth_[4096];
+static uint64_t wide_depth_h[1024];
 static uint32_t alive_count(const void* xv) {
     const node_t* x = xv;
     uint32_t a = 0;
@@ -157,13 +159,16 @@ int main(int argc, char** argv) {
     root->edges = e2 / 2;
     int sp = 1;
     node_t x;
+    depth_[0] = 0;
     while (sp > 0) {
-        x = stack_[--sp];
+        uint32_t dep = depth_[--sp];
+        x = stack_[sp];
         for (;;) {
             st_nodes++;
             {
                 uint32_t a = alive_count(&x);
                 st_alive_visit[a >= 512 ? 16 : a / 32]++;
+                if (a > 64) wide_depth_h[dep < 1023 ? dep : 1023]++;
             }
             if (reduce(&x, k)) break;
             if (x.edges == 0) { printf("cover found (yes-instance)\n"); return 0; }
@@ -223,10 +228,12 @@ int main(int argc, char** argv) {
                 uint64_t e = 0;
                 for (uint32_t w = 0; w < n; ++w) if (is_alive(&ch, w)) e += ch.d[w];
                 ch.edges = e / 2;
+                depth_[sp] = dep + 1;
                 stack_[sp++] = ch;
                 st_stored++;
             }
             remove_v(&x, v);
+            dep++;
         }
     }
     printf("nodes %lu rounds %lu branch %lu dead %lu stored %lu doom_at_round_start %lu (first round %lu)\n",
@@ -245,6 +252,8 @@ int main(int argc, char** argv) {
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_visit[i]);
     printf("\nalive at branch (x32):");
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_branch_h[i]);
+    printf("\nwide visits by depth:");
+    for (int i = 0; i < 1024; ++i) if (wide_depth_h[i]) printf(" %d:%lu", i, wide_depth_h[i]);
     printf("\ndead words hist:");
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_dead_hist[i]);
     printf("\n");
