@@ -146,6 +146,16 @@ __global__ void gather_records_kernel(const unsigned char* src, const uint32_t* 
     }
 }
 
+// Dynamic shared memory of the dense kernels (dense_scratch_base / dense_degree_base): the
+// adjacency bitmap, a W-word slot per warp, W x 32 scratch words per warp, and with
+// VCG_WIDE_SMEM the wide degrees (W x 32 words per warp, laid out after 8 warps of scratch).
+size_t dense_smem_bytes(uint32_t W, uint32_t warps) {
+    const size_t npad = 32 * (size_t)W;
+    const size_t base = W * npad * 4 + 8 * (size_t)W * 4;
+    return VCG_WIDE_SMEM ? base + 8 * (size_t)W * 32 * 4 + warps * (size_t)W * 32 * 4
+                         : base + warps * (size_t)W * 32 * 4;
+}
+
 uint32_t pick_w(uint32_t n) {
     if (n <= 128) return 4;
     if (n <= 256) return 8;
@@ -397,7 +407,7 @@ struct DenseRun {
         block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
         block = 32 * block_warps;
         // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-        smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + (size_t)block_warps * W * 32 * 4;
+        smem = dense_smem_bytes(W, block_warps);
         int per_sm = 1;
         switch (W) {
             case 4: per_sm = occupancy<4>(block, smem, s.instrument); break;
@@ -678,7 +688,7 @@ uint32_t full_device_workers(const Graph& g, int dev) {
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
     const uint32_t W = pick_w(g.n), npad = 32 * W, block = 256;
-    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + 8 * (size_t)W * 32 * 4;
+    const size_t smem = dense_smem_bytes(W, 8);
     int per_sm = 1;
     switch (W) {
         case 4: per_sm = occupancy<4>(block, smem, false); break;
@@ -903,7 +913,7 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
         g.dev[dev] = dg;
     }
     const DeviceGraph& dg = *g.dev[dev];
-    const size_t smem = (size_t)W * npad * 4 + 8 * (size_t)W * 4 + 8 * (size_t)W * 32 * 4;  // see dense_scratch_base
+    const size_t smem = dense_smem_bytes(W, 8);  // see dense_scratch_base
 
     // Levels stay on the device: per level only the flags come down and the gather list of
     // surviving children goes up; the final level is copied once.

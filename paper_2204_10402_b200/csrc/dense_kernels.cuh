@@ -119,6 +119,16 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
                  : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint2 ld_volatile_v2(const void* p) {
+    uint2 r;
+    asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -241,6 +251,9 @@ constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1;
 #define VCG_POLL_EVERY 8  // nodes between reads of the control line (power of two)
 #endif
 constexpr uint32_t kPoll = VCG_POLL_EVERY;
+#ifndef VCG_WIDE_SMEM
+#define VCG_WIDE_SMEM 1   // wide degrees in shared memory (fewer registers) instead of registers
+#endif
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -253,12 +266,29 @@ template <int W>
 __device__ __forceinline__ uint32_t dense_scratch_base(uint32_t wib) {
     return (W / 4) * (32 * W) * 4 + 8 * W + wib * W * 32;
 }
+// (VCG_WIDE_SMEM) per-warp degree words after the scratch words of 8 warps
+template <int W>
+__device__ __forceinline__ uint32_t dense_degree_base(uint32_t wib) {
+    return dense_scratch_base<W>(8) + wib * W * 32;
+}
 
 template <int W, bool INSTR>
 struct WarpNode {
     static constexpr bool kInstr = INSTR;
+    static constexpr int kPassUnroll = 1;  // (rolled: the wide pass body is large)
     static constexpr int Q = W / 4;  // uint4 groups per bitmap row
-    uint32_t d[W];                   // degree of vertex 32*i + lane (meaningless once removed)
+#if VCG_WIDE_SMEM
+    // degree of vertex 32*i + lane (meaningless once removed), in the warp's shared slots: the
+    // wide layout then holds no degree registers, so the kernel's register budget (and with
+    // it the occupancy of the compact hot path) is set by the compact layout
+    uint32_t dsb;                    // u32 index of this warp's W x 32 degree words
+    __device__ __forceinline__ uint32_t& D(int i) const {
+        return reinterpret_cast<uint32_t*>(dense_smem)[dsb + i * 32 + lane];
+    }
+#else
+    mutable uint32_t d[W];           // degree of vertex 32*i + lane (meaningless once removed)
+    __device__ __forceinline__ uint32_t& D(int i) const { return d[i]; }
+#endif
     uint32_t alv;                    // bit i: vertex 32*i + lane is alive (not in the cover)
     uint32_t aw;                     // lane j < W: alive bitmap word j (vertices 32j..32j+31)
     uint32_t nt;                     // bit i: vertex 32*i + lane has degree two and was found
@@ -298,7 +328,7 @@ struct WarpNode {
         for (int q = 0; q < Q; ++q) {
             const uint4 r = grp(q, u);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) d[4 * q + c] -= (comp(r, c) >> lane) & 1u;
+            for (int c = 0; c < 4; ++c) D(4 * q + c) -= (comp(r, c) >> lane) & 1u;
         }
         // (no verdict to invalidate: a cached non-triangle verdict is consulted only at degree
         // two, and a degree never rises, so once it leaves two the stale bit is never read)
@@ -314,7 +344,7 @@ struct WarpNode {
     __device__ __forceinline__ uint32_t eq_mask(uint32_t c) const {
         uint32_t m = 0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) m |= (d[i] == c ? 1u : 0u) << i;
+        for (int i = 0; i < W; ++i) m |= (D(i) == c ? 1u : 0u) << i;
         return m & alv;
     }
     // Alive vertices of degree > lim: the sign of lim - d (both < 2^16) funnel-shifted into the
@@ -322,7 +352,7 @@ struct WarpNode {
     __device__ __forceinline__ uint32_t above_mask(uint32_t lim) const {
         uint32_t m = 0;
 #pragma unroll
-        for (int i = W - 1; i >= 0; --i) m = __funnelshift_l(lim - d[i], m, 1);
+        for (int i = W - 1; i >= 0; --i) m = __funnelshift_l(lim - D(i), m, 1);
         return m & alv;
     }
     // pass 1, 2: degree == c; pass 3: degree > c
@@ -359,8 +389,8 @@ struct WarpNode {
         uint32_t m = above;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
-            const bool two = d[i] == 2u && !((nt >> i) & 1u);
-            m |= (d[i] == 1u || two ? 1u : 0u) << i;
+            const bool two = D(i) == 2u && !((nt >> i) & 1u);
+            m |= (D(i) == 1u || two ? 1u : 0u) << i;
         }
         return __any_sync(FULL, (m & alv) != 0);
     }
@@ -369,7 +399,7 @@ struct WarpNode {
         uint32_t mx = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i)
-            mx = max(mx, alive(i) ? ((d[i] << 11) | (2047u - (32u * i + lane))) : 0u);
+            mx = max(mx, alive(i) ? ((D(i) << 11) | (2047u - (32u * i + lane))) : 0u);
         mx = __reduce_max_sync(FULL, mx);
         return 2047u - (mx & 2047u);
     }
@@ -392,8 +422,8 @@ struct WarpNode {
         m1 = m2 = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i) {
-            m1 |= (d[i] == 1u ? 1u : 0u) << i;
-            m2 |= (d[i] == 2u ? 1u : 0u) << i;
+            m1 |= (D(i) == 1u ? 1u : 0u) << i;
+            m2 |= (D(i) == 2u ? 1u : 0u) << i;
         }
         m1 &= alv;
         m2 &= alv & ~nt;
@@ -470,7 +500,7 @@ struct WarpNode {
             // such a survivor stays above iff it loses less than its headroom
 #pragma unroll
             for (int i = 0; i < W; ++i)
-                scratch(i) = ((keepm >> i) & 1u) ? (uint32_t)max((int)(d[i] - lim), 0) : 0u;
+                scratch(i) = ((keepm >> i) & 1u) ? (uint32_t)max((int)(D(i) - lim), 0) : 0u;
         }
         uint32_t above = 0;
         // rolled pass over vertex words
@@ -501,7 +531,7 @@ struct WarpNode {
         for (int i = 0; i < W; ++i) {
             const bool keep = (keepm >> i) & 1u;
             const uint32_t lost = scratch(i);  // own writes: no sync needed
-            const uint32_t nd = keep ? d[i] - lost : 0xFFFFu;
+            const uint32_t nd = keep ? D(i) - lost : 0xFFFFu;
             esum += keep ? nd : 0u;
             if (i & 1) packed[i / 2] |= nd << 16;
             else packed[i / 2] = nd;
@@ -530,7 +560,7 @@ struct WarpNode {
         uint32_t packed[W / 2];
 #pragma unroll
         for (int i = 0; i < W; ++i) {
-            const uint32_t h = alive(i) ? d[i] : 0xFFFFu;
+            const uint32_t h = alive(i) ? D(i) : 0xFFFFu;
             if (i & 1) packed[i / 2] |= h << 16;
             else packed[i / 2] = h;
         }
@@ -566,7 +596,7 @@ struct WarpNode {
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             const uint32_t x = (i & 1) ? (packed[i / 2] >> 16) : (packed[i / 2] & 0xFFFFu);
-            d[i] = x;
+            D(i) = x;
             alv |= (x != 0xFFFFu ? 1u : 0u) << i;
         }
         rebuild_aw();
@@ -603,6 +633,11 @@ constexpr uint32_t kCompactRecordBytes = 32 + 32 * 16 + 32 * 4;
 template <bool INSTR>
 struct CompactNode {
     static constexpr bool kInstr = INSTR;
+#ifndef VCG_COMPACT_PASS_UNROLL
+#define VCG_COMPACT_PASS_UNROLL 3
+#endif
+    // the three passes unrolled: candidate selection and pass tests become compile-time
+    static constexpr int kPassUnroll = VCG_COMPACT_PASS_UNROLL;
     static constexpr int H = 2;          // slots per lane
     // Candidate masks are WARP-UNIFORM 64-bit slot masks built with two ballots: counting and
     // "first candidate >= pos" are then plain ALU work on every lane, with no reductions.
@@ -834,7 +869,7 @@ __device__ __forceinline__ void reduce_node(N& x, int B, Cnt& st) {
         if (!N::any(m1 | m2 | above)) break;  // the final no-change round
         bool removed = false;  // a removal happened since the round-start masks
         bool changed = false;
-#pragma unroll 1
+#pragma unroll (N::kPassUnroll)
         for (int pass = 1; pass <= 3; ++pass) {
             long long t0 = N::kInstr ? clock64() : 0;
             uint32_t c = pass;  // passes 1, 2: the degree; pass 3: the limit
@@ -878,7 +913,7 @@ __device__ __forceinline__ void reduce_node(N& x, int B, Cnt& st) {
                         if (!tri) x.mark_nt(v);
                     }
                 }
-#pragma unroll 1
+#pragma unroll (N::kPassUnroll == 1 ? 1 : 2)
                 for (int t = 0; t < 2; ++t) {
                     const int u = t ? u1 : u0;
                     if (u < 0) break;
@@ -1020,8 +1055,8 @@ enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
 
 template <int W, bool INSTR, bool MULTI>
 #ifndef VCG_MINB16
-#define VCG_MINB16 2  // CTAs of 8 warps per SM targeted by the W=16 register allocation
-#endif               // (with the compact layout: 2 → 128 regs, C5 12.5 ms; 3 → 80 + spills, 13.1)
+#define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
+#endif               // (wide degrees in smem: 3 → 80 regs, C5 10.2 ms; 2 → 127 regs, 10.8 ms; 4 → 64 + spills, 12.9)
 #ifndef VCG_MINB8
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
@@ -1036,23 +1071,37 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     __syncthreads();
     if (worker >= a.workers) return;
 
-    const unsigned long long t_start = globaltimer();
-    const long long c_start = clock64();
+    // start times live in the warp's scratch words while the search runs (read only for
+    // timeout checks and the final stats): two fewer 64-bit registers on the hot path
+    // (the warp's W-word slot between the bitmap and the scratch words; W >= 4)
+    unsigned long long* const t0s = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
+    if (lane == 0) {
+        t0s[0] = globaltimer();
+        t0s[1] = (unsigned long long)clock64();
+    }
+    __syncwarp();
+#define t_start (t0s[0])
+#define c_start ((long long)t0s[1])
     // The current node is WIDE (x: all 32*W vertex slots) until at most 64 vertices are alive,
     // then COMPACT (y: renumbered induced subgraph, see CompactNode).
     WarpNode<W, INSTR> x;
     x.ssb = dense_scratch_base<W>(wib);
+#if VCG_WIDE_SMEM
+    x.dsb = dense_degree_base<W>(wib);
+#endif
     x.lane = lane;
     CompactNode<INSTR> y;
     y.lane = lane;
     bool compact = false;
-    uint32_t* const sb = reinterpret_cast<uint32_t*>(dense_smem) + x.ssb;  // warp scratch
-    const uint32_t vec16 = (uint32_t)(a.entry_bytes / 16);
+    // (derived on use rather than held in registers: the hot path's register budget sets the
+    // occupancy)
+#define sb (reinterpret_cast<uint32_t*>(dense_smem) + x.ssb)  // warp scratch
+#define vec16 ((uint32_t)(a.entry_bytes / 16))
     Counters32 st;
     Ctl* ctl = a.ctl;
-    WStats* const my_stats = a.stats + worker;
-    unsigned char* const my_stack =
-        a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes;
+#define my_stats (a.stats + worker)
+#define my_stack (a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes)
     // The local stack is a ring [base, base + sp) so its oldest entry can be donated.
     uint32_t base = 0, sp = 0;
     auto slot_at = [&](uint32_t i) {
@@ -1067,8 +1116,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     int B = bound_of(a.pvc, a.k, best);  // prune once |S| > B
     uint32_t qsize = 0, polls = kPoll - 1;  // (the first node polls)
     bool poll = false;
-    uint4 h = make_uint4(0, 0, 0, 0);
-    unsigned long long hw = 0;
+    uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
+    uint32_t hw = 0;             // worklist size
     // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
     const bool multi = MULTI;  // linked shards (a separate instantiation: the single-shard
                                // kernel carries none of the peer code)
@@ -1083,7 +1132,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
                 best = min(best, __shfl_sync(FULL, h.x, 0));
                 B = bound_of(0, 0, best);
             }
-            qsize = __shfl_sync(FULL, (uint32_t)hw, 0);
+            qsize = __shfl_sync(FULL, hw, 0);
             if (multi) starve = __shfl_sync(FULL, hp, 0);
         }
         const bool prune = n.doom || prune_at(B, n.cc, n.edges);
@@ -1294,8 +1343,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         // issued here and consumed after the reduction.
         poll = (++polls & (kPoll - 1)) == 0;
         if (poll && lane == 0) {
-            h = ld_volatile_v4(ctl);
-            hw = ld_relaxed_u64(&ctl->work);
+            h = ld_volatile_v2(ctl);
+            hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
             if (multi) {  // one peer per poll, round robin: is it below its donation threshold?
                 const uint32_t p = (a.rank + 1 + probe++ % (a.world - 1)) % a.world;
                 hp = (uint32_t)ld_relaxed_sys_u64(&a.peers[p].ctl->work) < a.threshold ? p : a.world;
@@ -1351,6 +1400,12 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
 #pragma unroll
         for (int p = 0; p < 10; ++p) my_stats->phase[p] = INSTR ? st.phase[p] : 0ull;
     }
+#undef t_start
+#undef c_start
+#undef sb
+#undef vec16
+#undef my_stats
+#undef my_stack
 }
 
 // ------------------------------------------------------------------ frontier expansion
@@ -1381,6 +1436,9 @@ __global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     WarpNode<W, false> x;
     x.ssb = dense_scratch_base<W>(threadIdx.x >> 5);
+#if VCG_WIDE_SMEM
+    x.dsb = dense_degree_base<W>(threadIdx.x >> 5);
+#endif
     x.lane = lane;
     Counters st;
 #pragma unroll 1
