@@ -372,3 +372,19 @@ def test_sharded_timeout_cancels_every_shard():
     g = load_config("c5")
     r = solve_sharded(g, "pvc", 482, devices=(0, 0), timeout_s=0.002)
     assert r["status"] == "timeout"
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c5"])
+def test_compact_and_wide_layouts_visit_the_same_tree(config_golden, name):
+    """The compact renumbering keeps the id order, so the node counts of the all-wide layout
+    (engine="dense-wide") and the default one equal the reference's on PVC no-instances, and the
+    1-warp seq order is the reference's node for node in both."""
+    g = load_config(name)
+    gold = config_golden[name]
+    for engine in ("dense", "dense-wide"):
+        r = vc.solve_pvc(g, gold["pvc_no_k"], strategy="gpu", engine=engine)
+        assert not r["feasible"] and r["nodes_total"] == gold["pvc_no_nodes"], (engine, r["nodes_total"])
+    if name != "c5":
+        for engine in ("dense", "dense-wide"):
+            s = vc.solve_mvc(g, strategy="seq", engine=engine)
+            assert s["size"] == gold["mvc"] and sum(s["worker_nodes"]) == gold["seq_nodes"], engine

@@ -239,3 +239,30 @@ def test_report_metrics_semantics():
     assert ratios == [1.0, 1.0]  # metrics.cpp:32-36
     _, shares = collect_metrics([5], [10] + [0] * 9, 40)
     assert shares["worklist_remove"] == 0.25 and abs(shares["other"] - 0.75) < 1e-12
+
+
+# ---- multi-shard session API: argument validation happens before any device work ----------
+
+def test_session_open_validates_like_solve():
+    import ctypes as C
+    from paper_2204_10402_b200 import _native, _params
+    g = petersen()
+    h = C.c_void_p()
+    p, _ = _params("pvc", 0, "gpu", 0, 4096, 0.5, 8, 50, None, None)
+    with pytest.raises(ValueError, match="k >= 1"):
+        _native.check(_native.lib.vcg_session_open(g._h, C.byref(p), 0, C.byref(h)))
+    p, _ = _params("pvc", 3, "seq", 1, 4096, 0.5, 8, 50, None, None)
+    with pytest.raises(ValueError, match="hybrid"):
+        _native.check(_native.lib.vcg_session_open(g._h, C.byref(p), 0, C.byref(h)))
+    p, _ = _params("mvc", 0, "gpu", 0, 4096, 1.5, 8, 50, None, None)
+    with pytest.raises(ValueError, match="threshold_fraction"):
+        _native.check(_native.lib.vcg_session_open(g._h, C.byref(p), 0, C.byref(h)))
+    with pytest.raises(ValueError):
+        _native.check(_native.lib.vcg_session_link_local(None, 2))
+    assert _native.lib.vcg_session_handle_bytes() == 3 * 64  # three cudaIpcMemHandle_t
+
+
+def test_shard_rejects_k_zero():
+    from paper_2204_10402_b200.shards import Shard
+    with pytest.raises(ValueError, match="k >= 1"):
+        Shard(petersen(), "pvc", 0)
