@@ -8,8 +8,9 @@ step = one complete exact solve (the whole 21,461,369-node search tree; answer "
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 runs under torchrun, one process per GPU: a deterministic device frontier expansion on
-every rank, then each rank's share on its own GPU (strong scaling, max-over-ranks time).
+N>1 runs under torchrun, one process per GPU: rank 0's shard starts from the root, every GPU's
+device worklist is linked to the others' through CUDA IPC / NVLink P2P, and workers donate
+work straight into a starving peer's ring (strong scaling, max-over-ranks time).
 `--impl reference` times the reference's own CPU solver (oracle/_ref/libvcref.so, run_hybrid
 with every host thread) on bounded samples of the same workload.
 """
@@ -42,7 +43,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--frontier-per-rank", type=int, default=1024)
+    ap.add_argument("--frontier-per-rank", type=int, default=0,
+                    help="N>1: 0 = rank 0 starts from the root and the linked device worklists "
+                         "spread the work; else a deterministic frontier of this many nodes per rank")
     ap.add_argument("--ref-sample-s", type=float, default=0.0,
                     help="reference arm: seconds per bounded sample (0 = sized to the run)")
     return ap.parse_args()
@@ -201,9 +204,17 @@ def main():
     import paper_2204_10402_b200 as vc
     from paper_2204_10402_b200.configs import load_config
 
+    # VCG_BENCH_SAME_DEVICE=1 (test hook): every rank on cuda:0 — exercises the N>1 path on a
+    # one-GPU box (time-sliced processes; not a scaling number)
+    same = os.environ.get("VCG_BENCH_SAME_DEVICE") == "1"
+    if same:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         xg = dist.new_group(backend="gloo")
     stream = torch.cuda.Stream()  # the library launches on this stream; events bracket it
     g = load_config("c5")
@@ -245,7 +256,7 @@ def main():
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([elapsed_ms], device="cuda")
+        t = torch.tensor([elapsed_ms], device="cpu" if same else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
 
@@ -299,12 +310,33 @@ def main():
                              "time_to_solution_s": e2e_s / args.e2e_steps}
     else:
         line_extra["rank_nodes"] = results[-1]["rank_nodes"]
+        line_extra["rank_donated_peer"] = results[-1].get("rank_donated_peer")
         line_extra["frontier_nodes"] = results[-1]["frontier_nodes"]
         line_extra["frontier_size"] = results[-1]["frontier_size"]
-        line_extra["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": None,
-                             "d2h_bytes_per_step": None,
-                             "note": "multi-GPU steps run through the public API "
-                                     "(solve_distributed) end to end"}
+        # e2e: every rank builds a fresh graph from host CSR arrays each step and runs the
+        # public multi-GPU call (frontier expansion, IPC rendezvous, linked shards, readback);
+        # wall time, max over ranks
+        from paper_2204_10402_b200.distributed import solve_distributed
+        off, nbr = g.csr()
+        e2e_nodes, e2e_h2d, e2e_d2h = 0, 0, 0
+        dist.barrier(group=xg)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            gh = vc.from_csr(n, m, off, nbr)
+            r = solve_distributed(gh, "pvc", K_NO, exchange_group=xg, device=local,
+                                  frontier_per_rank=args.frontier_per_rank)
+            e2e_nodes += r["nodes_total"]
+            e2e_h2d += r.get("h2d_bytes", 0)
+            e2e_d2h += r.get("d2h_bytes", 0)
+            del gh
+        e2e_s = torch.tensor([time.perf_counter() - t0])
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX, group=xg)
+        e2e_s = float(e2e_s.item())
+        line_extra["e2e"] = {"value": e2e_nodes / e2e_s, "unit": UNIT,
+                             "h2d_bytes_per_step": e2e_h2d // args.e2e_steps,
+                             "d2h_bytes_per_step": e2e_d2h // args.e2e_steps,
+                             "ms_per_step": e2e_s * 1e3 / args.e2e_steps,
+                             "time_to_solution_s": e2e_s / args.e2e_steps}
 
     if rank != 0:
         return
@@ -317,7 +349,8 @@ def main():
         "config": {"workload": WORKLOAD, "n": n, "m": m, "k": K_NO,
                    "nodes_per_step": nodes_per_step, "strategy": "gpu",
                    "l2": "flushed between timed steps (256 MB memset)",
-                   "parallelism": "1 GPU" if world == 1 else f"{world} GPUs, frontier shards"},
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"{world} GPUs, one shard each, worklists linked over NVLink P2P (CUDA IPC)"},
         "clocks": clk,
         "gpu_launches": sum(r["kernel_launches"] for r in results),
     }

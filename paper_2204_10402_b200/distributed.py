@@ -230,19 +230,22 @@ def _solve_peer(graph, mode, k, group, frontier_per_rank, device, expander, shar
                 solve_kw):
     """solve_distributed with device-linked worklists (see shards.py)."""
     import torch.distributed as dist
-    from .shards import Shard, combine
+    from .shards import Shard, combine, root_frontier
     Shard = shard_factory or Shard
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     t0 = time.perf_counter()
-    fr = expander(graph, mode, k, frontier_per_rank * world, device=device)
-    fr["frontier_size"] = int(len(fr["seeds"]))
+    if frontier_per_rank:
+        fr = expander(graph, mode, k, frontier_per_rank * world, device=device)
+        fr["frontier_size"] = int(len(fr["seeds"]))
+    else:  # rank 0 starts from the root; donation between GPUs spreads the work
+        fr = root_frontier(graph, mode, k)
     share = fr["seeds"][rank::world]
     parts = []
-    if not (mode == "pvc" and fr["found"]) and len(fr["seeds"]):
+    if not (mode == "pvc" and fr["found"]) and (len(fr["seeds"]) or not frontier_per_rank):
         extra = {} if mode == "pvc" else {"initial_best": fr["best"]}
         shard = Shard(graph, mode, k, seeds=share if len(share) else None, device=device,
-                      **extra, **solve_kw)
+                      with_root=not frontier_per_rank and rank == 0, **extra, **solve_kw)
         try:
             handles = [None] * world
             dist.all_gather_object(handles, shard.export(), group=group)
@@ -256,9 +259,10 @@ def _solve_peer(graph, mode, k, group, frontier_per_rank, device, expander, shar
         finally:
             shard.close()
         keep = ("size", "feasible", "cover", "cover_from_search", "status", "worker_nodes",
-                "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches")
+                "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches",
+                "h2d_bytes", "d2h_bytes", "greedy_size")
         parts = [None] * world
-        dist.all_gather_object(parts, {x: mine[x] for x in keep}, group=group)
+        dist.all_gather_object(parts, {x: mine.get(x, 0) for x in keep}, group=group)
     out = combine(graph, mode, fr, parts, (time.perf_counter() - t0) * 1e3)
     out["exchange"] = "peer"
     return out

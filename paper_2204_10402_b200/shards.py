@@ -129,36 +129,55 @@ def combine(graph, mode, frontier, parts, wall_ms):
                 rank_donated_peer=[r["donated_peer"] for r in parts],
                 worker_nodes=[w for r in parts for w in r["worker_nodes"]],
                 kernel_launches=frontier["kernel_launches"] + sum(r["kernel_launches"] for r in parts),
-                greedy_size=frontier["greedy_size"], wall_ms=wall_ms)
+                greedy_size=max([frontier["greedy_size"]] + [r.get("greedy_size", 0) for r in parts]),
+                wall_ms=wall_ms,
+                h2d_bytes=sum(r.get("h2d_bytes", 0) for r in parts),
+                d2h_bytes=sum(r.get("d2h_bytes", 0) for r in parts))
 
 
-def solve_sharded(graph, mode="pvc", k=0, *, devices=(0, 0), frontier_per_shard=64,
+def root_frontier(graph, mode, k):
+    """No expansion: shard 0 starts from the root and device-to-device donation spreads the
+    work (the greedy cover is the MVC certificate to beat, as in run_hybrid)."""
+    from . import greedy_approx
+    size, cover = greedy_approx(graph) if mode == "mvc" else (0, [])  # (PVC: the shards report it)
+    return dict(seeds=np.zeros((0, 2 + graph.num_vertices), np.uint32), nodes=0, levels=0,
+                best=size if mode == "mvc" else k, greedy_size=size, found=False,
+                cover=[c + graph.id_base for c in cover] if mode == "mvc" else [],
+                kernel_launches=0, frontier_size=0)
+
+
+def solve_sharded(graph, mode="pvc", k=0, *, devices=(0, 0), frontier_per_shard=0,
                   workers_per_shard=None, skew=False, **kw):
     """All shards in this process, linked through device memory (peer access between GPUs).
 
-    The shards start from a deterministic frontier (``vcg_expand_frontier``) dealt round
-    robin. Several shards on one device must share it: ``workers_per_shard`` defaults to an
-    equal split of the full-device worker count, so every shard stays resident at once.
-    ``skew=True`` deals the whole frontier to shard 0: the others only ever work on what is
-    donated to them (a test of the device-to-device exchange)."""
+    ``frontier_per_shard=0`` (default): shard 0 starts from the root, the others empty, and
+    donation spreads the work. Otherwise the shards start from a deterministic frontier
+    (``vcg_expand_frontier``, one launch per tree level) dealt round robin; ``skew=True`` deals
+    it all to shard 0. Several shards on one device must share it: ``workers_per_shard``
+    defaults to an equal split of the full-device worker count, so every shard stays resident
+    at once."""
     from .distributed import expand_frontier
     world = len(devices)
     if world < 1:
         raise ValueError("need at least one shard")
     t0 = time.perf_counter()
-    fr = expand_frontier(graph, mode, k, frontier_per_shard * world, device=devices[0])
-    fr["frontier_size"] = int(len(fr["seeds"]))
+    if frontier_per_shard:
+        fr = expand_frontier(graph, mode, k, frontier_per_shard * world, device=devices[0])
+        fr["frontier_size"] = int(len(fr["seeds"]))
+    else:
+        fr = root_frontier(graph, mode, k)
     decided = mode == "pvc" and fr["found"]
     if workers_per_shard is None:
         same = max(devices.count(d) for d in set(devices))
         workers_per_shard = 0 if same == 1 else device_workers(graph, devices[0]) // same
     shards, parts = [], []
     try:
-        if not decided and len(fr["seeds"]):
+        if not decided and (len(fr["seeds"]) or not frontier_per_shard):
             extra = {} if mode == "pvc" else {"initial_best": fr["best"]}
             for r, dev in enumerate(devices):
                 share = (fr["seeds"] if r == 0 else fr["seeds"][:0]) if skew else fr["seeds"][r::world]
                 shards.append(Shard(graph, mode, k, seeds=share if len(share) else None,
+                                    with_root=not frontier_per_shard and r == 0,
                                     device=dev, workers=workers_per_shard, **extra, **kw))
             link_local(shards)
             for s in shards:

@@ -179,15 +179,17 @@ class FakeShard:
     """Records what solve_distributed asks of a shards.Shard (no device)."""
     log = None
 
-    def __init__(self, graph, mode, k, *, seeds=None, device=0, **kw):
+    def __init__(self, graph, mode, k, *, seeds=None, device=0, with_root=False, **kw):
         self.seeds = seeds
         self.kw = kw
+        self.with_root = with_root
         self.rank = None
-        FakeShard.log["opened"] = dict(n=0 if seeds is None else len(seeds), kw=sorted(kw))
+        FakeShard.log["opened"] = dict(n=0 if seeds is None else len(seeds), kw=sorted(kw),
+                                       with_root=with_root)
 
     @property
     def work_units(self):
-        return 0 if self.seeds is None else len(self.seeds)
+        return len(self.seeds) if self.seeds is not None else int(self.with_root)
 
     def export(self):
         return bytes([dist.get_rank()]) * 8
@@ -208,12 +210,12 @@ class FakeShard:
         FakeShard.log["closed"] = True
 
 
-def worker_peer(rank, world, port, out):
+def worker_peer(rank, world, port, out, fpr=2):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2204_10402_b200.distributed import solve_distributed
     FakeShard.log = {}
-    r = solve_distributed(FakeGraph(), "pvc", 4, frontier_per_rank=2, expander=fake_expander,
+    r = solve_distributed(FakeGraph(), "pvc", 4, frontier_per_rank=fpr, expander=fake_expander,
                           shard_factory=FakeShard, exchange="peer", timeout_s=5)
     out.put((rank, r, FakeShard.log))
     dist.destroy_process_group()
@@ -238,6 +240,7 @@ def test_peer_exchange_rendezvous_on_three_ranks():
     shares = [len(range(rk, total, world)) for rk in range(world)]
     for rank, (r, log) in got.items():
         assert log["opened"]["n"] == shares[rank] and log["opened"]["kw"] == ["timeout_s"]
+        assert not log["opened"]["with_root"]
         assert log["link"]["world"] == world and log["link"]["rank"] == rank
         assert log["link"]["handles"] == [bytes([q]) * 8 for q in range(world)]  # rank order
         assert log["link"]["units"] == shares
@@ -246,3 +249,26 @@ def test_peer_exchange_rendezvous_on_three_ranks():
         assert r["nodes_total"] == 100 + 10 * total
         assert r["rank_nodes"] == [10 * n for n in shares]
         assert r["rank_donated_peer"] == [1] * world
+
+
+def test_peer_exchange_root_only_start():
+    """frontier_per_rank=0: no expansion; rank 0 starts from the root, the others empty (the
+    linked worklists spread the work)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=worker_peer, args=(r, world, port, q, 0)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in range(world):
+        rank, r, log = q.get(timeout=120)
+        got[rank] = (r, log)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (r, log) in got.items():
+        assert log["opened"]["n"] == 0 and log["opened"]["with_root"] == (rank == 0)
+        assert log["link"]["units"] == [1, 0]
+        assert r["frontier_nodes"] == 0 and r["nodes_total"] == 10

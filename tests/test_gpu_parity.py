@@ -337,12 +337,15 @@ def test_sharded_pvc_pair_exact(config_golden, name, skew):
     from paper_2204_10402_b200.shards import solve_sharded
     g = load_config(name)
     gold = config_golden[name]
-    no = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=(0, 0), skew=skew, timeout_s=60)
+    fps = 64 if skew else 0  # skew: a frontier dealt to shard 0; else the root on shard 0
+    no = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=(0, 0), skew=skew,
+                       frontier_per_shard=fps, timeout_s=60)
     assert no["status"] == "complete" and not no["feasible"]
     assert no["nodes_total"] == gold["pvc_no_nodes"], (no["nodes_total"], no["rank_nodes"])
-    if skew and no["rank_nodes"]:  # shard 1 starts empty: all it visits was donated to it
+    if name == "c1":  # shard 1 starts empty: all it visits was donated to it (C3 is too small)
         assert no["rank_nodes"][1] > 0, no["rank_nodes"]
-    yes = solve_sharded(g, "pvc", gold["mvc"], devices=(0, 0), skew=skew, timeout_s=60)
+    yes = solve_sharded(g, "pvc", gold["mvc"], devices=(0, 0), skew=skew,
+                        frontier_per_shard=fps, timeout_s=60)
     assert yes["feasible"] and len(yes["cover"]) <= gold["mvc"]
     assert vc.verify_cover(g, yes["cover"])
 
@@ -360,11 +363,12 @@ def test_sharded_c5_no_instance(config_golden):
     from paper_2204_10402_b200.shards import solve_sharded
     gold = config_golden["c5"]
     g = load_config("c5")
-    r = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=(0, 0), frontier_per_shard=256,
-                      timeout_s=120)
-    assert r["status"] == "complete" and not r["feasible"]
-    assert r["nodes_total"] == gold["pvc_no_nodes"]
-    assert min(r["rank_nodes"]) > 0
+    for fps, devices in ((256, (0, 0)), (0, (0, 0)), (0, (0, 0, 0, 0))):
+        r = solve_sharded(g, "pvc", gold["pvc_no_k"], devices=devices, frontier_per_shard=fps,
+                          timeout_s=120)
+        assert r["status"] == "complete" and not r["feasible"]
+        assert r["nodes_total"] == gold["pvc_no_nodes"]
+        assert min(r["rank_nodes"]) > 0 and sum(r["rank_donated_peer"]) > 0, r["rank_nodes"]
 
 
 def test_sharded_timeout_cancels_every_shard():

@@ -7,8 +7,9 @@ from paper_2204_10402_b200.shards import solve_sharded
 g = load_config("c5")
 r = vc.solve_pvc(g, 482, strategy="gpu")
 print("single", r["nodes_total"], round(r["device_ms"], 2))
-for devs, skew, fps, frac in [((0,), False, 64, 0.5), ((0, 0), False, 256, 0.5), ((0, 0), True, 256, 0.5),
-                              ((0, 0), False, 256, 0.05), ((0, 0, 0, 0), False, 256, 0.5)]:
+for devs, skew, fps, frac in [((0,), False, 0, 0.5), ((0, 0), False, 0, 0.5), ((0, 0), False, 256, 0.5),
+                              ((0, 0), True, 256, 0.5), ((0, 0, 0, 0), False, 0, 0.5),
+                              ((0,) * 8, False, 0, 0.5)]:
     for _ in range(2):
         r = solve_sharded(g, "pvc", 482, devices=devs, skew=skew, frontier_per_shard=fps, threshold_fraction=frac)
     print(json.dumps(dict(devs=len(devs), skew=skew, fps=fps, frac=frac, nodes=r["nodes_total"], rank_nodes=r["rank_nodes"],
