@@ -1356,10 +1356,16 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         if (st.nodes >= a.flush_every) {
             int stop = 0;
             if (lane == 0) {
-                const unsigned long long tot =
-                    atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes) + st.nodes;
-                if (a.node_budget && tot > a.node_budget) stop = 2;
-                else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) stop = 1;
+                // (without a node budget the total is never read back: a fire-and-forget
+                // reduction, no round trip to the contended counter)
+                if (a.node_budget) {
+                    const unsigned long long tot =
+                        atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes) + st.nodes;
+                    if (tot > a.node_budget) stop = 2;
+                } else {
+                    atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes);
+                }
+                if (!stop && a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) stop = 1;
                 if (stop) {
                     atomicCAS(&ctl->status, 0, stop);
                     cancel_all(a);

@@ -392,3 +392,34 @@ def test_compact_and_wide_layouts_visit_the_same_tree(config_golden, name):
         for engine in ("dense", "dense-wide"):
             s = vc.solve_mvc(g, strategy="seq", engine=engine)
             assert s["size"] == gold["mvc"] and sum(s["worker_nodes"]) == gold["seq_nodes"], engine
+
+
+def _phat_complement(n, a, b, seed):
+    """Complement of a p_hat-style random graph (vertex weights U[a, b], edge iff U < mean)."""
+    rng = np.random.default_rng(seed)
+    pw = a + (b - a) * rng.random(n)
+    adj = rng.random((n, n)) < (pw[:, None] + pw[None, :]) / 2
+    iu = np.triu_indices(n, 1)
+    keep = ~adj[iu]
+    return vc.make_graph(n, list(zip(iu[0][keep].tolist(), iu[1][keep].tolist())))
+
+
+@pytest.mark.parametrize("n,a,b", [(200, 0.25, 0.75), (600, 0.05, 0.3), (900, 0.0, 0.3)])
+def test_dense_widths_8_and_32_against_the_oracle(oracle, n, a, b):
+    """The W = 8 (n <= 256) and W = 32 (n <= 1024) kernels: MVC size, the PVC no-instance node
+    count and the 1-warp seq order equal the oracle's (the reference restatement)."""
+    from oracle.oracle import CSR
+    g = _phat_complement(n, a, b, 1)
+    off, nbr = g.csr()
+    csr = CSR(n, g.num_edges, off, nbr)
+    want = oracle.solve_seq(csr)
+    no = oracle.solve_seq(csr, pvc=True, k=want["size"] - 1)
+    assert not no["feasible"]
+    r = vc.solve_mvc(g, strategy="gpu")
+    assert r["size"] == want["size"] and r["engine"] == 1
+    check_cover(g, r)
+    for engine in ("dense", "dense-wide"):
+        p = vc.solve_pvc(g, want["size"] - 1, strategy="gpu", engine=engine)
+        assert not p["feasible"] and p["nodes_total"] == no["nodes"], (engine, p["nodes_total"], no["nodes"])
+    s = vc.solve_mvc(g, strategy="seq")
+    assert s["size"] == want["size"] and sum(s["worker_nodes"]) == want["nodes"]
