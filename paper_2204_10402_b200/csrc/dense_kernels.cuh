@@ -107,7 +107,6 @@ struct DenseArgs {
     // multi-shard solves (world > 1): every shard's exchange memory, this shard's index
     const PeerRef* peers;
     uint32_t world, rank;
-    int no_root;                 // this shard starts with an empty worklist
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -337,10 +336,9 @@ struct WarpNode {
         cc += 1;
         edges -= du;
     }
-    // First alive vertex v >= pos with lo <= d[v] <= hi at this moment — exactly the next vertex
-    // the reference's ascending pass would act on. -1 if none.
-    // Bit-sliced: each lane builds the mask of its own candidates (bit i = vertex 32*i + lane),
-    // and one REDUX picks the smallest id — no per-word ballots, no branches.
+    // Candidate masks are bit-sliced: each lane builds the mask of its own candidates (bit i =
+    // vertex 32*i + lane); first_in's one REDUX then picks the smallest id >= pos — exactly the
+    // next vertex the reference's ascending pass would act on.
     __device__ __forceinline__ uint32_t eq_mask(uint32_t c) const {
         uint32_t m = 0;
 #pragma unroll
@@ -355,11 +353,7 @@ struct WarpNode {
         for (int i = W - 1; i >= 0; --i) m = __funnelshift_l(lim - D(i), m, 1);
         return m & alv;
     }
-    // pass 1, 2: degree == c; pass 3: degree > c
-    __device__ __forceinline__ int find_first(int pos, int pass, uint32_t c, uint32_t skip) const {
-        return first_in((pass == 3 ? above_mask(c) : eq_mask(c)) & ~skip, pos);
-    }
-    // smallest vertex id >= pos in the bit-sliced candidate mask m (bit i = vertex 32*i + lane)
+    // smallest vertex id >= pos in the bit-sliced candidate mask m; -1 if none
     __device__ __forceinline__ int first_in(uint32_t m, int pos) const {
         const uint32_t pi = (uint32_t)pos >> 5;
         m &= lane >= (pos & 31) ? (FULL << pi) : (pi + 1 < 32 ? FULL << (pi + 1) : 0u);
@@ -379,20 +373,6 @@ struct WarpNode {
         const int j1 = w0b ? j0 : __ffs(b2) - 1;
         const uint32_t w1 = w0b ? w0b : __shfl_sync(FULL, xl, j1 & 31);
         p1 = (w0b || b2) ? 32 * j1 + __ffs(w1) - 1 : -1;
-    }
-    // Number of alive vertices of degree > lim (degree > lim >= 0 implies degree > 0).
-    __device__ __forceinline__ uint32_t count_above(uint32_t lim) const {
-        return __reduce_add_sync(FULL, __popc(above_mask(lim)));
-    }
-    // Can any rule fire? (an alive vertex of degree 1 or 2, or one in `above`)
-    __device__ __forceinline__ bool any_candidate(uint32_t above) const {
-        uint32_t m = above;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            const bool two = D(i) == 2u && !((nt >> i) & 1u);
-            m |= (D(i) == 1u || two ? 1u : 0u) << i;
-        }
-        return __any_sync(FULL, (m & alv) != 0);
     }
     // search_node.cpp:34-46: smallest id among alive vertices of maximum degree
     __device__ __forceinline__ uint32_t argmax() const {
