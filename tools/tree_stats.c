@@ -118,6 +118,8 @@ static int reduce(node_t* x, uint32_t k) {
 
 static node_t stack_[4096];
 static uint32_t depth_[4096];
+static uint32_t pw_[4096], pc_[4096];  /* wide / compact visits on the root path */
+static uint64_t best_w, best_c, best_cost;
 static uint64_t wide_depth_h[1024];
 static uint32_t alive_count(const void* xv) {
     const node_t* x = xv;
@@ -162,6 +164,7 @@ int main(int argc, char** argv) {
     depth_[0] = 0;
     while (sp > 0) {
         uint32_t dep = depth_[--sp];
+        uint32_t pw = pw_[sp], pc = pc_[sp];
         x = stack_[sp];
         for (;;) {
             st_nodes++;
@@ -169,6 +172,9 @@ int main(int argc, char** argv) {
                 uint32_t a = alive_count(&x);
                 st_alive_visit[a >= 512 ? 16 : a / 32]++;
                 if (a > 64) wide_depth_h[dep < 1023 ? dep : 1023]++;
+                if (a > 64) pw++; else pc++;
+                uint64_t cost = 8ull * pw + pc;
+                if (cost > best_cost) { best_cost = cost; best_w = pw; best_c = pc; }
             }
             if (reduce(&x, k)) break;
             if (x.edges == 0) { printf("cover found (yes-instance)\n"); return 0; }
@@ -229,6 +235,8 @@ int main(int argc, char** argv) {
                 for (uint32_t w = 0; w < n; ++w) if (is_alive(&ch, w)) e += ch.d[w];
                 ch.edges = e / 2;
                 depth_[sp] = dep + 1;
+                pw_[sp] = pw;
+                pc_[sp] = pc;
                 stack_[sp++] = ch;
                 st_stored++;
             }
@@ -252,6 +260,7 @@ int main(int argc, char** argv) {
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_visit[i]);
     printf("\nalive at branch (x32):");
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_branch_h[i]);
+    printf("\ncritical path (8 x wide + compact): %lu wide + %lu compact visits", best_w, best_c);
     printf("\nwide visits by depth:");
     for (int i = 0; i < 1024; ++i) if (wide_depth_h[i]) printf(" %d:%lu", i, wide_depth_h[i]);
     printf("\ndead words hist:");
