@@ -64,7 +64,7 @@ def csr_of(graph):
 # ---------------------------------------------------------------- clocks during the timed region
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
 
     def __init__(self, index):
         self.index = index
@@ -78,7 +78,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
