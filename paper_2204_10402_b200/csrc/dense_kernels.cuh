@@ -952,6 +952,20 @@ __device__ __noinline__ void cancel_all_(Ctl* ctl, const PeerRef* peers, uint32_
 }
 #define cancel_all(a) cancel_all_((a).ctl, (a).peers, (a).world, (a).rank)
 
+// Waits until ring slot `publish` is free for ticket `pos` (its previous lap's reader released
+// it). After a cancel that reader may have left for good, so the wait gives up when `cancel`
+// is raised (returns false: the caller keeps its record and leaves at its next poll).
+__device__ __noinline__ bool wait_slot_free(const unsigned long long* publish,
+                                            unsigned long long pos, const uint32_t* cancel,
+                                            bool sys) {
+#pragma unroll 1
+    for (uint32_t spin = 0;; ++spin) {
+        if ((sys ? ld_acquire_sys_u64(publish) : ld_acquire_u64(publish)) == pos) return true;
+        if ((spin & 15) == 15 && *reinterpret_cast<const volatile uint32_t*>(cancel)) return false;
+        __nanosleep(32);
+    }
+}
+
 // Copies one node record (either layout) through L2: `vec16` 16-byte vectors spread over the
 // warp's lanes.
 __device__ __forceinline__ void copy_record_raw(const unsigned char* src, unsigned char* dst,
@@ -963,8 +977,9 @@ __device__ __forceinline__ void copy_record_raw(const unsigned char* src, unsign
 
 // Work donation between shards (cold): reserve a slot in peer `pr`'s ring, copy the record at
 // `src` into it over NVLink / IPC, publish it with a system-scope release. Warp-collective.
-__device__ __noinline__ bool donate_to_peer(const PeerRef* pr, Ctl* ctl0, uint32_t capacity,
-                                            uint32_t ring_mask, unsigned long long entry_bytes,
+__device__ __noinline__ bool donate_to_peer(const PeerRef* pr, Ctl* ctl0, Ctl* own,
+                                            uint32_t capacity, uint32_t ring_mask,
+                                            unsigned long long entry_bytes,
                                             const unsigned char* src, int lane) {
     uint32_t* const gactive = &ctl0->gactive;
     unsigned long long pos = 0;
@@ -984,9 +999,10 @@ __device__ __noinline__ bool donate_to_peer(const PeerRef* pr, Ctl* ctl0, uint32
     if (!__shfl_sync(FULL, ok, 0)) return false;
     pos = __shfl_sync(FULL, pos, 0);
     unsigned long long* publish = pr->seq + (pos & ring_mask);
-    if (lane == 0)
-        while (ld_acquire_sys_u64(publish) != pos) __nanosleep(64);
-    __syncwarp();
+    int freed = 1;
+    if (lane == 0 && ld_acquire_sys_u64(publish) != pos)
+        freed = wait_slot_free(publish, pos, &own->cancel, true);
+    if (!__shfl_sync(FULL, freed, 0)) return false;
     copy_record_raw(src, pr->wl + (pos & ring_mask) * entry_bytes, (uint32_t)(entry_bytes / 16), lane);
     __syncwarp();
     if (lane == 0) st_release_sys_u64(publish, pos + 1);
@@ -1168,15 +1184,15 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
             unsigned long long seen = 0;
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
+            if (lane == 0 && ok) {
+                st.max_queue = max(st.max_queue, (uint32_t)seen);
+                // the slot is free once the previous lap's reader released it
+                if (ld_acquire_u64(a.seq + (pos & a.ring_mask)) != pos)  // (rarely not yet)
+                    ok = wait_slot_free(a.seq + (pos & a.ring_mask), pos, &ctl->cancel, false);
+            }
             if (__shfl_sync(FULL, ok, 0)) {
                 pos = __shfl_sync(FULL, pos, 0);
                 publish = a.seq + (pos & a.ring_mask);
-                if (lane == 0) {
-                    st.max_queue = max(st.max_queue, (uint32_t)seen);
-                    // the slot is free once the previous lap's reader released it
-                    while (ld_acquire_u64(publish) != pos) __nanosleep(32);
-                }
-                __syncwarp();
                 unsigned char* dst = a.wl + (pos & a.ring_mask) * a.entry_bytes;
                 if (oldest) {
                     copy_record_raw(slot_at(0), dst, vec16, lane);
@@ -1191,7 +1207,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         if (multi && !publish && starve < a.world && sp > 0 && !a.seq_mode) {
             // Work donation between shards: a peer below its threshold gets this worker's
             // oldest stacked node, written straight into its ring slot over NVLink / IPC.
-            if (donate_to_peer(a.peers + starve, a.peers[0].ctl, a.capacity, a.ring_mask,
+            if (donate_to_peer(a.peers + starve, a.peers[0].ctl, a.ctl, a.capacity, a.ring_mask,
                                a.entry_bytes, slot_at(0), lane)) {
                 base = base + 1 == a.stack_bound ? 0 : base + 1;
                 --sp;

@@ -802,14 +802,15 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         if (!a.seq_mode && qsize < a.threshold) {
             if (tid == 0) {
                 const unsigned long long old = atomicAdd(&ctl->work, ONE_PENDING | 1ull);
-                const int ok = (uint32_t)old < a.capacity;
+                int ok = (uint32_t)old < a.capacity;
                 if (!ok) {
                     atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
                 } else {
                     st.max_queue = max(st.max_queue, (unsigned long long)((uint32_t)old + 1));
                     sh.pos = atomicAdd(&ctl->tail, 1ull);
-                    unsigned long long* p = a.seq + (sh.pos & a.ring_mask);
-                    while (ld_acquire_u64(p) != sh.pos) __nanosleep(32);
+                    // (gives up after a cancel: the previous lap's reader may have left)
+                    if (ld_acquire_u64(a.seq + (sh.pos & a.ring_mask)) != sh.pos)
+                        ok = wait_slot_free(a.seq + (sh.pos & a.ring_mask), sh.pos, &ctl->cancel, false);
                 }
                 sh.outcome = ok;
             }
