@@ -423,3 +423,19 @@ def test_dense_widths_8_and_32_against_the_oracle(oracle, n, a, b):
         assert not p["feasible"] and p["nodes_total"] == no["nodes"], (engine, p["nodes_total"], no["nodes"])
     s = vc.solve_mvc(g, strategy="seq")
     assert s["size"] == want["size"] and sum(s["worker_nodes"]) == want["nodes"]
+
+
+@pytest.mark.parametrize("capacity", [8, 64, 4096])
+def test_yes_instance_cancel_with_small_rings(config_golden, capacity):
+    """A PVC yes-instance cancels every worker while donations are in flight; with a small
+    ring the tickets wrap quickly, so donors must not wait for slots whose previous-lap
+    readers already left (regression: that wait used to hang the kernel)."""
+    gold = config_golden["c5"]
+    g = load_config("c5")
+    for _ in range(3):
+        y = vc.solve_pvc(g, gold["pvc_yes_k"], strategy="gpu", capacity=capacity)
+        assert y["feasible"] and y["size"] <= gold["pvc_yes_k"]
+        check_cover(g, y)
+    from paper_2204_10402_b200.shards import solve_sharded
+    r = solve_sharded(g, "pvc", gold["pvc_yes_k"], devices=(0, 0), capacity=capacity)
+    assert r["feasible"] and vc.verify_cover(g, r["cover"])
