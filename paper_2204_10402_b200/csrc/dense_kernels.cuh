@@ -253,6 +253,9 @@ constexpr uint32_t kPoll = VCG_POLL_EVERY;
 #ifndef VCG_WIDE_SMEM
 #define VCG_WIDE_SMEM 1   // wide degrees in shared memory (fewer registers) instead of registers
 #endif
+#ifndef VCG_FROM_WIDE_BALLOT
+#define VCG_FROM_WIDE_BALLOT 1  // compact conversion: rows by ballots over slots (see from_wide)
+#endif
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -788,6 +791,23 @@ struct CompactNode {
         ids = id0 | (id1 << 16);
         am = nalive >= 64 ? ~0ull : ((1ull << nalive) - 1ull);
         nt = 0;  // (verdicts are a cache: starting empty only re-runs tests)
+#if VCG_FROM_WIDE_BALLOT
+        // induced rows, one slot t at a time: lane l tests A[id_l][id_t] and A[id_{l+32}][id_t];
+        // by symmetry the two ballots are row t itself (uniform work, no per-bit loops)
+        r[0] = r[1] = 0;
+#pragma unroll 1
+        for (uint32_t t = 0; t < nalive; ++t) {
+            const uint32_t idt = sid[t];
+            const uint32_t wj = idt >> 5, bit = idt & 31u;
+            const bool b0 = id0 != 0xFFFFu && ((w.row_word(id0, wj) >> bit) & 1u);
+            const bool b1 = id1 != 0xFFFFu && ((w.row_word(id1, wj) >> bit) & 1u);
+            const unsigned long long row = ballot2(b0, b1);
+            if (lane == (int)(t & 31u)) {
+                if (t >> 5) r[1] = row;
+                else r[0] = row;
+            }
+        }
+#else
         // induced rows: compress row(id) over the alive set, word by word
         r[0] = r[1] = 0;
 #pragma unroll 1
@@ -806,6 +826,7 @@ struct CompactNode {
                 }
             }
         }
+#endif
         set_degrees();
     }
     // Word `lane` (< W) of the cover bitmap (vertices not alive), built in shared scratch.
