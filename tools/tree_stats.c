@@ -1,7 +1,7 @@
 /* tools/tree_stats.c — offline analysis (not product, not test): walks the C5 PVC tree in the
  * dense engine's order on the CPU (bitmap node, reference rule order, doom tests, doomed
  * children counted at birth) and prints where the per-node work goes, to evaluate kernel ideas
- * without GPU time.  Usage: tree_stats graph.clq k [complement]
+ * without GPU time.  Usage: tree_stats graph.clq k [complement] [node cap]
  */
 #include <stdint.h>
 #include <stdio.h>
@@ -168,6 +168,7 @@ int main(int argc, char** argv) {
         x = stack_[sp];
         for (;;) {
             st_nodes++;
+            if (argc > 4 && st_nodes >= (uint64_t)atoll(argv[4])) goto done;
             {
                 uint32_t a = alive_count(&x);
                 st_alive_visit[a >= 512 ? 16 : a / 32]++;
@@ -244,6 +245,7 @@ int main(int argc, char** argv) {
             dep++;
         }
     }
+done:
     printf("nodes %lu rounds %lu branch %lu dead %lu stored %lu doom_at_round_start %lu (first round %lu)\n",
            st_nodes, st_rounds, st_branch, st_dead, st_stored, st_doom_start, st_first_round_doom);
     printf("scans p1 %lu p2 %lu p3 %lu; removals p1 %lu p2 %lu p3 %lu\n", st_pass_scans[1],
