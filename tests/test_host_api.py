@@ -266,3 +266,28 @@ def test_shard_rejects_k_zero():
     from paper_2204_10402_b200.shards import Shard
     with pytest.raises(ValueError, match="k >= 1"):
         Shard(petersen(), "pvc", 0)
+
+
+def test_shard_combine_rules():
+    """shards.combine: PVC is feasible if any part found a cover; MVC keeps the smallest
+    certificate among the frontier's and the parts' search covers; node counts add up."""
+    from paper_2204_10402_b200.shards import combine
+    fr = dict(nodes=7, levels=2, found=False, cover=[0, 1, 2, 3], greedy_size=4,
+              kernel_launches=2, frontier_size=0)
+
+    def part(**kw):
+        d = dict(size=0, feasible=False, cover=[], cover_from_search=False, status="complete",
+                 worker_nodes=[5], nodes_total=5, device_ms=1.0, donated=1, donated_peer=0,
+                 kernel_launches=2, greedy_size=4)
+        d.update(kw)
+        return d
+    r = combine(None, "pvc", fr, [part(), part(feasible=True, cover=[1, 2], size=2)], 1.0)
+    assert r["feasible"] and r["cover"] == [1, 2] and r["size"] == 2
+    assert r["nodes_total"] == 7 + 10 and r["rank_nodes"] == [5, 5]
+    r = combine(None, "pvc", fr, [part(), part(status="timeout")], 1.0)
+    assert not r["feasible"] and r["size"] is None and r["status"] == "timeout"
+    r = combine(None, "mvc", fr, [part(size=3, cover=[0, 1, 2], cover_from_search=True, feasible=True),
+                                 part(size=4, cover=[4, 5, 6, 7], feasible=True)], 1.0)
+    assert r["size"] == 3 and r["cover"] == [0, 1, 2]
+    r = combine(None, "mvc", fr, [part(size=4, feasible=True)], 1.0)
+    assert r["size"] == 4 and r["cover"] == [0, 1, 2, 3]  # the frontier's (greedy) certificate
