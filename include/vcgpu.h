@@ -219,6 +219,10 @@ VCG_API int vcg_session_link_ipc(vcg_session* s, uint32_t world, uint32_t rank,
                                  const void* handles, const uint64_t* seeds_per_shard);
 VCG_API int vcg_session_link_local(vcg_session* const* shards, uint32_t world);
 VCG_API int vcg_session_launch(vcg_session* s);
+/* Fresh search state for the next solve of the same session (same graph and parameters):
+ * buffers, IPC mappings and links are kept. Every linked shard must reset (and the caller must
+ * synchronise: all reset before any launches) between two solves. */
+VCG_API int vcg_session_reset(vcg_session* s);
 VCG_API int vcg_session_wait(vcg_session* s, vcg_result* out);
 VCG_API void vcg_session_close(vcg_session* s);
 /* Workers (warps) of a full-device dense-engine solve of g on `device` (shards sharing a device

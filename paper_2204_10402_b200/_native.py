@@ -102,6 +102,7 @@ _SIGS = [
     ("vcg_session_link_ipc", C.c_int, [_VP, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     ("vcg_session_link_local", C.c_int, [C.c_void_p, C.c_uint32]),
     ("vcg_session_launch", C.c_int, [_VP]),
+    ("vcg_session_reset", C.c_int, [_VP]),
     ("vcg_session_wait", C.c_int, [_VP, C.POINTER(Result)]),
     ("vcg_session_close", None, [_VP]),
     ("vcg_device_workers", C.c_int, [_VP, C.c_int32, C.POINTER(C.c_uint32)]),

@@ -410,6 +410,15 @@ int vcg_session_link_local(vcg_session* const* shards, uint32_t world) {
     });
 }
 
+int vcg_session_reset(vcg_session* s) {
+    return guarded([&]() -> int {
+        if (!s) return fail(VCG_EINVAL, "null argument");
+        s->host->t0 = std::chrono::steady_clock::now();
+        vcg::session_reset(s->ses);
+        return VCG_OK;
+    });
+}
+
 int vcg_session_launch(vcg_session* s) {
     return guarded([&]() -> int {
         if (!s) return fail(VCG_EINVAL, "null argument");

@@ -211,9 +211,10 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
 }
 
 template <int W>
-int occupancy(uint32_t block, size_t smem, bool instr) {
+int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     int nb = 0;
-    auto k = instr ? dense_kernel<W, true, false> : dense_kernel<W, false, false>;
+    auto k = multi ? dense_kernel<W, false, true>
+                   : (instr ? dense_kernel<W, true, false> : dense_kernel<W, false, false>);
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)block, smem));
     return nb;
@@ -410,10 +411,10 @@ struct DenseRun {
         smem = dense_smem_bytes(W, block_warps);
         int per_sm = 1;
         switch (W) {
-            case 4: per_sm = occupancy<4>(block, smem, s.instrument); break;
-            case 8: per_sm = occupancy<8>(block, smem, s.instrument); break;
-            case 16: per_sm = occupancy<16>(block, smem, s.instrument); break;
-            default: per_sm = occupancy<32>(block, smem, s.instrument); break;
+            case 4: per_sm = occupancy<4>(block, smem, s.instrument, owned); break;
+            case 8: per_sm = occupancy<8>(block, smem, s.instrument, owned); break;
+            case 16: per_sm = occupancy<16>(block, smem, s.instrument, owned); break;
+            default: per_sm = occupancy<32>(block, smem, s.instrument, owned); break;
         }
         if (per_sm < 1) throw std::runtime_error("CUDA error: dense kernel cannot be resident");
         workers = s.workers;
@@ -442,9 +443,8 @@ struct DenseRun {
         cover_slots = reinterpret_cast<uint32_t*>(misc + sizeof(Ctl));
         stats = reinterpret_cast<WStats*>(misc + sizeof(Ctl) + slots_bytes);
 
-        // initial worklist content: the root (init_root, search_node.cpp:7-14), the seeds, or
-        // nothing (a shard with an empty share)
-        nseeds = s.num_seeds ? s.num_seeds : (s.no_root ? 0 : 1);
+        seed();
+        a = DenseArgs{};
         std::vector<unsigned char> recs(nseeds * entry);
         if (s.num_seeds) {
             for (uint64_t i = 0; i < nseeds; ++i) {
@@ -468,11 +468,6 @@ struct DenseRun {
         init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
         CUDA_CHECK(cudaGetLastError());
         out.launches += 2;  // init_seq_kernel + dense_kernel
-        CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
-        out.h2d_bytes += sizeof(hc) + recs.size();
-        if (owned) CUDA_CHECK(cudaStreamSynchronize(st));  // (peers may map it before launch)
-
-        a = DenseArgs{};
         a.at4 = dg.at4;
         a.n = g.n;
         a.npad = npad;
@@ -511,6 +506,54 @@ struct DenseRun {
         a.rank = 0;
     }
 
+    // The initial worklist and control state: the root (init_root, search_node.cpp:7-14), the
+    // seeds, or nothing (a shard with an empty share). Run again by reset() for the next solve
+    // of a persistent multi-shard session (buffers and peer mappings kept).
+    void seed() {
+        nseeds = s.num_seeds ? s.num_seeds : (s.no_root ? 0 : 1);
+        std::vector<unsigned char> recs(nseeds * entry);
+        if (s.num_seeds) {
+            for (uint64_t i = 0; i < nseeds; ++i) {
+                const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
+                pack_record(W, g.n, r[0], r[1], r + 2, recs.data() + i * entry);
+            }
+        } else if (nseeds) {
+            std::vector<uint32_t> deg(g.n);
+            for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
+            pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs.data());
+        }
+        std::memset(&hc, 0, sizeof(hc));
+        hc.best = s.best;
+        hc.head = 0;
+        hc.tail = nseeds;
+        hc.work = (nseeds << 32) | nseeds;
+        hc.best_owner = ~0ull;
+        hc.gactive = active_;  // (read from shard 0's copy only)
+        CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+        if (nseeds)
+            CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+        init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
+        CUDA_CHECK(cudaGetLastError());
+        out.launches += 2;  // init_seq_kernel + dense_kernel
+        CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
+        out.h2d_bytes += sizeof(hc) + recs.size();
+        if (owned) CUDA_CHECK(cudaStreamSynchronize(st));  // (peers may map it before launch)
+    }
+    uint32_t active_ = 0;  // multi-shard: shards with initial work (shard 0's gactive)
+
+    // Next solve of a persistent session: the same graph and parameters, fresh state.
+    void reset() {
+        CUDA_CHECK(cudaSetDevice(dev));
+        out = SolveOut();
+        out.engine = 1;
+        out.degree_bytes = 2;
+        out.n_padded = npad;
+        out.grid = grid;
+        out.block = block;
+        CUDA_CHECK(cudaEventRecord(evh, st));
+        seed();
+    }
+
     // Multi-shard: every shard's exchange memory (this one's included, at `rank`).
     void link(uint32_t world, uint32_t rank, const std::vector<PeerRef>& refs, uint32_t active) {
         CUDA_CHECK(cudaSetDevice(dev));
@@ -519,6 +562,7 @@ struct DenseRun {
         a.peers = peers_dev;
         a.world = world;
         a.rank = rank;
+        active_ = active;
         if (rank == 0)  // shard 0 holds the shard-activity count
             CUDA_CHECK(cudaMemcpy(&ctl->gactive, &active, 4, cudaMemcpyHostToDevice));
     }
@@ -681,6 +725,8 @@ void session_link_local(Session* const* shards, uint32_t world) {
 
 void session_launch(Session* ses) { ses->run->launch(); }
 
+void session_reset(Session* ses) { ses->run->reset(); }
+
 uint32_t full_device_workers(const Graph& g, int dev) {
     SolveSpec s;
     s.device = dev;
@@ -691,10 +737,10 @@ uint32_t full_device_workers(const Graph& g, int dev) {
     const size_t smem = dense_smem_bytes(W, 8);
     int per_sm = 1;
     switch (W) {
-        case 4: per_sm = occupancy<4>(block, smem, false); break;
-        case 8: per_sm = occupancy<8>(block, smem, false); break;
-        case 16: per_sm = occupancy<16>(block, smem, false); break;
-        default: per_sm = occupancy<32>(block, smem, false); break;
+        case 4: per_sm = occupancy<4>(block, smem, false, true); break;
+        case 8: per_sm = occupancy<8>(block, smem, false, true); break;
+        case 16: per_sm = occupancy<16>(block, smem, false, true); break;
+        default: per_sm = occupancy<32>(block, smem, false, true); break;
     }
     return (uint32_t)C.sms * per_sm * 8;
 }

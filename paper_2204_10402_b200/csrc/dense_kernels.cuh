@@ -1077,7 +1077,10 @@ template <int W, bool INSTR, bool MULTI>
 #ifndef VCG_MINB8
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
-__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB16 : 1))) dense_kernel(DenseArgs a) {
+#ifndef VCG_MINB_MULTI
+#define VCG_MINB_MULTI 3  // the multi-shard instantiation (W = 16)
+#endif
+__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : VCG_MINB16) : 1))) dense_kernel(DenseArgs a) {
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -1138,7 +1141,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
     // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
     const bool multi = MULTI;  // linked shards (a separate instantiation: the single-shard
                                // kernel carries none of the peer code)
-    uint32_t starve = a.world, hp = a.world, probe = 0;
+    uint32_t starve = a.world, hp = a.world, probe = 0, hpv = ~0u;
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto settle = [&](auto& n) -> int {
@@ -1362,9 +1365,17 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? VCG_MINB
         if (poll && lane == 0) {
             h = ld_volatile_v2(ctl);
             hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
-            if (multi) {  // one peer per poll, round robin: is it below its donation threshold?
-                const uint32_t p = (a.rank + 1 + probe++ % (a.world - 1)) % a.world;
-                hp = (uint32_t)ld_relaxed_sys_u64(&a.peers[p].ctl->work) < a.threshold ? p : a.world;
+            if (multi) {
+                // One peer per poll, round robin: is it below its donation threshold? The read
+                // crosses NVLink, so it is consumed one poll later (it has long arrived): the
+                // verdict on the previous probe's peer now, the next peer's read in flight.
+                if (probe) {
+                    const uint32_t p = (a.rank + 1 + (probe - 1) % (a.world - 1)) % a.world;
+                    hp = hpv < a.threshold ? p : a.world;
+                }
+                hpv = (uint32_t)ld_relaxed_sys_u64(
+                    &a.peers[(a.rank + 1 + probe % (a.world - 1)) % a.world].ctl->work);
+                ++probe;
             }
         }
 

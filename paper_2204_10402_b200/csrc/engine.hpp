@@ -84,6 +84,7 @@ void session_link_ipc(Session* ses, uint32_t world, uint32_t rank, const void* h
 // link shards living in this process (same or peer-accessible devices)
 void session_link_local(Session* const* shards, uint32_t world);
 void session_launch(Session* ses);                 // asynchronous
+void session_reset(Session* ses);                  // fresh state for the next solve (kept links)
 void session_wait(Session* ses, SolveOut& out);    // blocks, assembles the result
 void session_close(Session* ses);
 // Workers (warps) of a full-device dense solve of g: shards sharing a device split these.

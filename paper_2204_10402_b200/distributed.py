@@ -226,43 +226,79 @@ def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_p
                 exchange_rounds=mon.rounds, greedy_size=fr["greedy_size"])
 
 
+class PeerSolver:
+    """One rank's persistent shard for repeated multi-GPU solves of one (graph, mode, k): the
+    shard is opened, its CUDA IPC handles exchanged over the CPU group and the peers mapped
+    ONCE; every solve() then only resets the device state (all ranks reset before any launch),
+    launches, waits, and gathers the small per-rank results. Rank 0 starts from the root (or
+    from a deterministic frontier share, frontier_per_rank > 0)."""
+
+    def __init__(self, graph, mode, k, group, *, device=0, frontier_per_rank=0, expander=None,
+                 shard_factory=None, **solve_kw):
+        import torch.distributed as dist
+        from .shards import Shard, combine, root_frontier
+        self._combine = combine
+        Shard = shard_factory or Shard
+        self.graph, self.mode, self.k, self.group = graph, mode, k, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if frontier_per_rank:
+            fr = (expander or expand_frontier)(graph, mode, k, frontier_per_rank * self.world,
+                                               device=device)
+            fr["frontier_size"] = int(len(fr["seeds"]))
+        else:  # rank 0 starts from the root; donation between GPUs spreads the work
+            fr = root_frontier(graph, mode, k)
+        self.frontier = fr
+        share = fr["seeds"][self.rank::self.world]
+        self.decided = (mode == "pvc" and fr["found"]) or (frontier_per_rank and not len(fr["seeds"]))
+        self.shard = None
+        self.fresh = True
+        if self.decided:
+            return
+        extra = {} if mode == "pvc" else {"initial_best": fr["best"]}
+        self.shard = Shard(graph, mode, k, seeds=share if len(share) else None, device=device,
+                           with_root=not frontier_per_rank and self.rank == 0, **extra,
+                           **solve_kw)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.shard.export(), group=group)
+        units = [None] * self.world
+        dist.all_gather_object(units, self.shard.work_units, group=group)
+        self.shard.link_ipc(self.world, self.rank, handles, units)
+
+    def solve(self):
+        import torch.distributed as dist
+        t0 = time.perf_counter()
+        parts = []
+        if self.shard is not None:
+            if not self.fresh:
+                self.shard.reset()
+            self.fresh = False
+            dist.barrier(group=self.group)  # every shard (re)initialised before any launch
+            self.shard.launch()
+            mine = self.shard.wait()
+            keep = ("size", "feasible", "cover", "cover_from_search", "status", "worker_nodes",
+                    "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches",
+                    "h2d_bytes", "d2h_bytes", "greedy_size")
+            # (the gather is also the barrier that keeps every kernel done before any reset)
+            parts = [None] * self.world
+            dist.all_gather_object(parts, {x: mine.get(x, 0) for x in keep}, group=self.group)
+        out = self._combine(self.graph, self.mode, self.frontier, parts,
+                            (time.perf_counter() - t0) * 1e3)
+        out["exchange"] = "peer"
+        return out
+
+    def close(self):
+        if self.shard is not None:
+            self.shard.close()
+            self.shard = None
+
+
 def _solve_peer(graph, mode, k, group, frontier_per_rank, device, expander, shard_factory,
                 solve_kw):
-    """solve_distributed with device-linked worklists (see shards.py)."""
-    import torch.distributed as dist
-    from .shards import Shard, combine, root_frontier
-    Shard = shard_factory or Shard
-    rank = dist.get_rank(group)
-    world = dist.get_world_size(group)
-    t0 = time.perf_counter()
-    if frontier_per_rank:
-        fr = expander(graph, mode, k, frontier_per_rank * world, device=device)
-        fr["frontier_size"] = int(len(fr["seeds"]))
-    else:  # rank 0 starts from the root; donation between GPUs spreads the work
-        fr = root_frontier(graph, mode, k)
-    share = fr["seeds"][rank::world]
-    parts = []
-    if not (mode == "pvc" and fr["found"]) and (len(fr["seeds"]) or not frontier_per_rank):
-        extra = {} if mode == "pvc" else {"initial_best": fr["best"]}
-        shard = Shard(graph, mode, k, seeds=share if len(share) else None, device=device,
-                      with_root=not frontier_per_rank and rank == 0, **extra, **solve_kw)
-        try:
-            handles = [None] * world
-            dist.all_gather_object(handles, shard.export(), group=group)
-            units = [None] * world
-            dist.all_gather_object(units, shard.work_units, group=group)
-            shard.link_ipc(world, rank, handles, units)
-            dist.barrier(group=group)  # every shard linked (shard 0's count set) before launch
-            shard.launch()
-            mine = shard.wait()
-            dist.barrier(group=group)  # no peer unmaps while another kernel may still write
-        finally:
-            shard.close()
-        keep = ("size", "feasible", "cover", "cover_from_search", "status", "worker_nodes",
-                "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches",
-                "h2d_bytes", "d2h_bytes", "greedy_size")
-        parts = [None] * world
-        dist.all_gather_object(parts, {x: mine.get(x, 0) for x in keep}, group=group)
-    out = combine(graph, mode, fr, parts, (time.perf_counter() - t0) * 1e3)
-    out["exchange"] = "peer"
-    return out
+    """solve_distributed with device-linked worklists: a one-shot PeerSolver."""
+    ps = PeerSolver(graph, mode, k, group, device=device, frontier_per_rank=frontier_per_rank,
+                    expander=expander, shard_factory=shard_factory, **solve_kw)
+    try:
+        return ps.solve()
+    finally:
+        ps.close()

@@ -71,6 +71,10 @@ class Shard:
     def launch(self):
         _n.check(_lib.vcg_session_launch(self._h))
 
+    def reset(self):
+        """Fresh search state for another solve (buffers, IPC mappings and links kept)."""
+        _n.check(_lib.vcg_session_reset(self._h))
+
     def wait(self):
         from . import _result_dict
         r = _n.Result()
@@ -144,6 +148,48 @@ def root_frontier(graph, mode, k):
                 best=size if mode == "mvc" else k, greedy_size=size, found=False,
                 cover=[c + graph.id_base for c in cover] if mode == "mvc" else [],
                 kernel_launches=0, frontier_size=0)
+
+
+class ShardedSolver:
+    """Persistent in-process shards (several devices, or several shards of one device): opened
+    and linked once, then every solve() only resets the device state — the multi-shard setup
+    cost (buffers, links) is paid once, not per solve. Root start (shard 0), donation spreads
+    the work."""
+
+    def __init__(self, graph, mode="pvc", k=0, *, devices=(0, 0), workers_per_shard=None, **kw):
+        self.graph, self.mode, self.k = graph, mode, k
+        self.frontier = root_frontier(graph, mode, k)
+        if workers_per_shard is None:
+            same = max(devices.count(d) for d in set(devices))
+            workers_per_shard = 0 if same == 1 else device_workers(graph, devices[0]) // same
+        extra = {} if mode == "pvc" else {"initial_best": self.frontier["best"]}
+        self.shards = []
+        try:
+            for r, dev in enumerate(devices):
+                self.shards.append(Shard(graph, mode, k, with_root=r == 0, device=dev,
+                                         workers=workers_per_shard, **extra, **kw))
+            link_local(self.shards)
+        except Exception:
+            self.close()
+            raise
+        self.fresh = True
+
+    def solve(self):
+        t0 = time.perf_counter()
+        if not self.fresh:
+            for s in self.shards:  # (all reset before any launches)
+                s.reset()
+        self.fresh = False
+        for s in self.shards:
+            s.launch()
+        parts = [s.wait() for s in self.shards]
+        return combine(self.graph, self.mode, self.frontier, parts,
+                       (time.perf_counter() - t0) * 1e3)
+
+    def close(self):
+        for s in self.shards:
+            s.close()
+        self.shards = []
 
 
 def solve_sharded(graph, mode="pvc", k=0, *, devices=(0, 0), frontier_per_shard=0,

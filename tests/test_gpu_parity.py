@@ -439,3 +439,27 @@ def test_yes_instance_cancel_with_small_rings(config_golden, capacity):
     from paper_2204_10402_b200.shards import solve_sharded
     r = solve_sharded(g, "pvc", gold["pvc_yes_k"], devices=(0, 0), capacity=capacity)
     assert r["feasible"] and vc.verify_cover(g, r["cover"])
+
+
+def test_persistent_shards_solve_repeatedly(config_golden):
+    """ShardedSolver: shards linked once, reset between solves — every solve visits the
+    reference's tree exactly (the reset leaves no stale queue, counter or activity state)."""
+    from paper_2204_10402_b200.shards import ShardedSolver
+    gold = config_golden["c5"]
+    g = load_config("c5")
+    ss = ShardedSolver(g, "pvc", gold["pvc_no_k"], devices=(0, 0))
+    try:
+        for _ in range(4):
+            r = ss.solve()
+            assert r["status"] == "complete" and not r["feasible"]
+            assert r["nodes_total"] == gold["pvc_no_nodes"], r["rank_nodes"]
+    finally:
+        ss.close()
+    c1 = load_config("c1")
+    ss = ShardedSolver(c1, "mvc", devices=(0, 0, 0))
+    try:
+        for _ in range(3):
+            r = ss.solve()
+            assert r["size"] == config_golden["c1"]["mvc"] and vc.verify_cover(c1, r["cover"])
+    finally:
+        ss.close()
