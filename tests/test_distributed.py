@@ -198,7 +198,10 @@ class FakeShard:
         FakeShard.log["link"] = dict(world=world, rank=rank, handles=handles, units=list(units))
 
     def launch(self):
-        FakeShard.log["launched"] = True
+        FakeShard.log["launched"] = FakeShard.log.get("launched", 0) + 1
+
+    def reset(self):
+        FakeShard.log["resets"] = FakeShard.log.get("resets", 0) + 1
 
     def wait(self):
         n = self.work_units
@@ -272,3 +275,36 @@ def test_peer_exchange_root_only_start():
         assert log["opened"]["n"] == 0 and log["opened"]["with_root"] == (rank == 0)
         assert log["link"]["units"] == [1, 0]
         assert r["frontier_nodes"] == 0 and r["nodes_total"] == 10
+
+
+def worker_persistent(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_10402_b200.distributed import PeerSolver
+    FakeShard.log = {}
+    ps = PeerSolver(FakeGraph(), "pvc", 4, None, shard_factory=FakeShard)
+    rs = [ps.solve() for _ in range(3)]
+    ps.close()
+    out.put((rank, rs, dict(FakeShard.log)))
+    dist.destroy_process_group()
+
+
+def test_peer_solver_links_once_and_resets_between_solves():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=worker_persistent, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = {}
+    for _ in range(world):
+        rank, rs, log = q.get(timeout=120)
+        got[rank] = (rs, log)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (rs, log) in got.items():
+        assert log["launched"] == 3 and log["resets"] == 2 and log["closed"]
+        assert log["link"]["units"] == [1, 0]  # linked once (the log keeps the one call)
+        assert all(r["nodes_total"] == 10 and r["exchange"] == "peer" for r in rs)
