@@ -1078,7 +1078,8 @@ template <int W, bool INSTR, bool MULTI>
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
 #ifndef VCG_MINB_MULTI
-#define VCG_MINB_MULTI 3  // the multi-shard instantiation (W = 16)
+#define VCG_MINB_MULTI 2  // the multi-shard instantiation (W = 16): 128 registers, no spills
+                          // (2 shards on one B200: 14.1 ms vs 16.0 ms at 3 CTAs/SM with spills)
 #endif
 __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : VCG_MINB16) : 1))) dense_kernel(DenseArgs a) {
     constexpr int Q = W / 4;
@@ -1204,7 +1205,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
         }
         const bool oldest = a.donate_oldest && sp > 0;
-        if (!a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
+        // a drained peer shard comes first (at start-up only rank 0 holds any work)
+        const bool urgent = multi && (starve >> 16) && sp > 0 && !a.seq_mode;
+        if (!urgent && !a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
             unsigned long long seen = 0;
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
@@ -1228,10 +1231,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 ++st.donated;
             }
         }
-        if (multi && !publish && starve < a.world && sp > 0 && !a.seq_mode) {
+        if (multi && !publish && (starve & 0xFFFFu) < a.world && sp > 0 && !a.seq_mode) {
             // Work donation between shards: a peer below its threshold gets this worker's
             // oldest stacked node, written straight into its ring slot over NVLink / IPC.
-            if (donate_to_peer(a.peers + starve, a.peers[0].ctl, a.ctl, a.capacity, a.ring_mask,
+            if (donate_to_peer(a.peers + (starve & 0xFFFFu), a.peers[0].ctl, a.ctl, a.capacity, a.ring_mask,
                                a.entry_bytes, slot_at(0), lane)) {
                 base = base + 1 == a.stack_bound ? 0 : base + 1;
                 --sp;
@@ -1371,7 +1374,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 // verdict on the previous probe's peer now, the next peer's read in flight.
                 if (probe) {
                     const uint32_t p = (a.rank + 1 + (probe - 1) % (a.world - 1)) % a.world;
-                    hp = hpv < a.threshold ? p : a.world;
+                    // (a drained peer — empty queue — outranks this shard's own worklist)
+                    hp = hpv < a.threshold ? (p | (hpv == 0 ? 0x10000u : 0u)) : a.world;
                 }
                 hpv = (uint32_t)ld_relaxed_sys_u64(
                     &a.peers[(a.rank + 1 + probe % (a.world - 1)) % a.world].ctl->work);
