@@ -445,29 +445,6 @@ struct DenseRun {
 
         seed();
         a = DenseArgs{};
-        std::vector<unsigned char> recs(nseeds * entry);
-        if (s.num_seeds) {
-            for (uint64_t i = 0; i < nseeds; ++i) {
-                const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
-                pack_record(W, g.n, r[0], r[1], r + 2, recs.data() + i * entry);
-            }
-        } else if (nseeds) {
-            std::vector<uint32_t> deg(g.n);
-            for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
-            pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs.data());
-        }
-        std::memset(&hc, 0, sizeof(hc));
-        hc.best = s.best;
-        hc.head = 0;
-        hc.tail = nseeds;
-        hc.work = (nseeds << 32) | nseeds;
-        hc.best_owner = ~0ull;
-        CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
-        if (nseeds)
-            CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
-        init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
-        CUDA_CHECK(cudaGetLastError());
-        out.launches += 2;  // init_seq_kernel + dense_kernel
         a.at4 = dg.at4;
         a.n = g.n;
         a.npad = npad;
