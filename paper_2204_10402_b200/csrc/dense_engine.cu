@@ -204,7 +204,9 @@ template <int W, bool INSTR>
 void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s) {
     if (INSTR && a.world > 1)
         throw std::invalid_argument("instrumented runs are single-shard");
-    auto k = a.world > 1 ? dense_kernel<W, false, true> : dense_kernel<W, INSTR, false>;
+    auto k = a.world > 1 ? dense_kernel<W, false, true>
+             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true>
+                                            : dense_kernel<W, INSTR, false>;
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, block, smem, s>>>(a);
     CUDA_CHECK(cudaGetLastError());

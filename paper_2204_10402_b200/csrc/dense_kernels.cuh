@@ -1070,7 +1070,7 @@ __device__ __noinline__ bool record_cover_(Ctl* ctl, uint32_t* cover_slots, vola
 
 enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
 
-template <int W, bool INSTR, bool MULTI>
+template <int W, bool INSTR, bool MULTI, bool ONEW = false>
 #ifndef VCG_MINB16
 #define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
 #endif               // (wide degrees in smem: 3 → 80 regs, C5 10.2 ms; 2 → 127 regs, 10.8 ms; 4 → 64 + spills, 12.9)
@@ -1140,6 +1140,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
     uint32_t hw = 0;             // worklist size
     // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
+    // (the one-worker strategies — seq, StackOnly — are a separate instantiation: the hybrid
+    // kernel carries none of their marker / replay code)
+    const bool seq_mode_ = ONEW && a.seq_mode;
+    const bool stackonly_ = ONEW && a.stackonly;
     const bool multi = MULTI;  // linked shards (a separate instantiation: the single-shard
                                // kernel carries none of the peer code)
     uint32_t starve = a.world, hp = a.world, probe = 0, hpv = ~0u;
@@ -1181,7 +1185,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         long long tb = INSTR ? clock64() : 0;
         // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
         // child (0 = remove v_max, 1 = remove N(v_max), scheduler.cpp:303-309), nothing deferred
-        const bool replaying = a.stackonly && replay < a.depth;
+        const bool replaying = stackonly_ && replay < a.depth;
         const bool right = replaying && ((subtree >> replay) & 1ull);
         replay += replaying;
         unsigned char* child = nullptr;
@@ -1199,15 +1203,15 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
             // budget) must not count it — so they stack a 16-byte marker in its place instead.
             dead = n.template child_pass<true>(c, B);
-            if (!a.seq_mode) {
+            if (!seq_mode_) {
                 st.nodes += dead;
                 st.dooms += dead;
             }
         }
         const bool oldest = a.donate_oldest && sp > 0;
         // a drained peer shard comes first (at start-up only rank 0 holds any work)
-        const bool urgent = multi && (starve >> 16) && sp > 0 && !a.seq_mode;
-        if (!urgent && !a.seq_mode && qsize < a.threshold && (oldest || !dead)) {
+        const bool urgent = multi && (starve >> 16) && sp > 0 && !seq_mode_;
+        if (!urgent && !seq_mode_ && qsize < a.threshold && (oldest || !dead)) {
             unsigned long long seen = 0;
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
@@ -1231,7 +1235,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 ++st.donated;
             }
         }
-        if (multi && !publish && (starve & 0xFFFFu) < a.world && sp > 0 && !a.seq_mode) {
+        if (multi && !publish && (starve & 0xFFFFu) < a.world && sp > 0 && !seq_mode_) {
             // Work donation between shards: a peer below its threshold gets this worker's
             // oldest stacked node, written straight into its ring slot over NVLink / IPC.
             if (donate_to_peer(a.peers + (starve & 0xFFFFu), a.peers[0].ctl, a.ctl, a.capacity, a.ring_mask,
@@ -1243,7 +1247,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
             starve = a.world;  // (re-armed by the next poll)
         }
-        if (build && (!dead || a.seq_mode)) {
+        if (build && (!dead || seq_mode_)) {
             if (!child) {
                 child = slot_at(sp);
                 ++sp;
@@ -1278,7 +1282,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             if (sp > 0) {
                 --sp;
                 src = slot_at(sp);
-            } else if (a.stackonly) {
+            } else if (stackonly_) {
                 // stackonly_worker (scheduler.cpp:279-281): claim the next sub-tree id and
                 // replay its root path from the root record (ring slot 0, never consumed)
                 unsigned long long t = 0;
