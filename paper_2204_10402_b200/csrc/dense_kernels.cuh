@@ -7,19 +7,24 @@
 // remove_*_into_cover (search_node.cpp:16-46), GlobalWorklist (worklist.cpp:11-48).
 //
 // Layout:
-//  * one WARP = one worker; the current node's degree array lives in REGISTERS: lane l holds
-//    the degrees of vertices 32*i + l (i < W), u32, kRemoved = 0xFFFFFFFF;
+//  * one WARP = one worker. A node is WIDE (WarpNode: lane l owns vertices 32*i + l, i < W; the
+//    u32 degrees in the warp's shared-memory slots, alive / verdict bits in registers) until at
+//    most 64 vertices are alive, then COMPACT (CompactNode: the alive vertices renumbered in id
+//    order, each lane holding the induced 64-bit adjacency rows and degrees of its two slots in
+//    registers, warp-uniform 64-bit candidate masks). 97% of C5's visits are compact.
 //  * the read-only graph is an adjacency bitmap staged once per CTA in shared memory, word j of
 //    vertex w's row at uint4 group (j/4)*npad + w (column-coalesced, row-broadcast);
-//  * deferred nodes are 16 + 64*W + 128 byte records: {cover_count, edge_count, 0, 0}, lane-major
-//    u16 degrees (lane l's W entries contiguous), then one word per lane of cached degree-two
-//    non-triangle verdicts; they live in a per-warp stack in HBM or in the device ring.
+//  * deferred nodes are records {cover_count, edge_count, kind, 0} + a wide body (lane-major
+//    u16 degrees and one word per lane of cached degree-two non-triangle verdicts) or a compact
+//    body (alive / verdict masks, induced rows, slot ids); they live in a per-warp ring stack
+//    in HBM (L2-resident top) or in the device worklist ring.
+//  * both layouts run the same reduce_node: the reference's rule order, bit for bit.
 //
-// Instruction footprint matters more than instruction count here: with the rule code inlined
-// at every call site the W=16 kernel was 128 KB of SASS and 64% of warp stalls were
-// `no_instruction`. Every primitive below therefore has ONE call site in the node loop
-// (remove_vertex: two), the three rule passes share one rolled loop with a range predicate, and
-// loops that do not index the register array are not unrolled.
+// Instruction footprint matters here: with the rule code inlined at every call site the wide
+// W=16 kernel was 128 KB of SASS and 64% of warp stalls were `no_instruction`. Every primitive
+// therefore has one call site per layout, the three rule passes share one rolled loop, cold
+// paths (cover recording, peer donation, cancel broadcast, slot waits) are out of line, and the
+// multi-shard and one-worker (seq / StackOnly) variants are separate instantiations.
 #pragma once
 
 #include <cuda_runtime.h>
