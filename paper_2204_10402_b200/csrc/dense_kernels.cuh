@@ -944,6 +944,22 @@ template <class Cnt>
 __device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int B, Cnt& st) {
     reduce_node(*this, B, st);
 }
+// The wide reduction out of line (VCG_WIDE_NOINLINE): the wide layout is the cold one, and its
+// rule code inlined next to the compact hot loop costs instruction-cache misses. Counter deltas
+// come back by value (a reference to the kernel's counters would move them to local memory).
+struct RuleDeltas {
+    uint32_t rounds, rm1, rm2, rmh;
+};
+template <int W>
+__device__ __noinline__ RuleDeltas wide_reduce(WarpNode<W, false>& x, int B) {
+    CountersT<uint32_t> c;
+    reduce_node(x, B, c);
+    return RuleDeltas{c.rounds, c.rm1, c.rm2, c.rmh};
+}
+#ifndef VCG_WIDE_NOINLINE
+#define VCG_WIDE_NOINLINE 1
+#endif
+
 template <bool INSTR>
 template <class Cnt>
 __device__ __forceinline__ void CompactNode<INSTR>::reduce(int B, Cnt& st) {
@@ -1155,7 +1171,17 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto settle = [&](auto& n) -> int {
-        n.reduce(B, st);
+        if constexpr (VCG_WIDE_NOINLINE && !INSTR &&
+                      std::is_same<typename std::remove_reference<decltype(n)>::type,
+                                   WarpNode<W, INSTR>>::value) {
+            const RuleDeltas dl = wide_reduce<W>(n, B);
+            st.rounds += dl.rounds;
+            st.rm1 += dl.rm1;
+            st.rm2 += dl.rm2;
+            st.rmh += dl.rmh;
+        } else {
+            n.reduce(B, st);
+        }
         if (poll) {
             if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
             if (!a.pvc) {
