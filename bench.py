@@ -64,7 +64,8 @@ def csr_of(graph):
 # ---------------------------------------------------------------- clocks during the timed region
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms; the samples inside the timed
+    region (mark) are the ones reported."""
 
     def __init__(self, index):
         self.index = index
@@ -88,7 +89,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, t0, t1):
+        """The timed region [t0, t1] (perf_counter): only samples read inside it (plus the first
+        after it, which covers its tail) are reported. The sampler is started before the
+        warm-up so that nvidia-smi's start-up does not eat into a short timed region."""
+        self.window = (t0, t1)
 
     def stop(self):
         if not self.proc:
@@ -100,7 +107,13 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for _, ln in self.lines]
+        win = getattr(self, "window", None)
+        if win:
+            inside = [ln for t, ln in self.lines if win[0] <= t <= win[1]]
+            after = [ln for t, ln in self.lines if t > win[1]][:1]
+            lines = inside + after or lines[-1:]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -236,19 +249,20 @@ def main():
             return r
         return peer.solve()
 
+    clocks = ClockSampler(local)  # (started before the warm-up; see ClockSampler.mark)
+    clocks.start()
     for _ in range(args.warmup):
         r = step()
         assert not r["feasible"], "C5 k=482 must be infeasible"
         with torch.cuda.stream(stream):
             flush.zero_()  # (the first fill pays torch's lazy kernel load: keep it out of the timing)
 
-    clocks = ClockSampler(local)
-    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     results = []
+    t_wall0 = time.perf_counter()
     with torch.cuda.stream(stream):
         ev0.record(stream)
         for _ in range(args.steps):
@@ -256,6 +270,7 @@ def main():
             flush.zero_()  # L2 flush between timed steps (inside the bracket; ~0.05 ms)
         ev1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark(t_wall0, time.perf_counter())
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
