@@ -239,7 +239,7 @@ def main():
         # one persistent shard per rank: IPC handles exchanged and peers mapped once; a step
         # resets the device state, launches, waits and gathers (graph resident, like N=1)
         from paper_2204_10402_b200.distributed import PeerSolver
-        peer = PeerSolver(g, "pvc", K_NO, xg, device=local,
+        peer = PeerSolver(g, "pvc", K_NO, xg, device=local, detail=False,
                           frontier_per_rank=args.frontier_per_rank)
 
     def step():

@@ -234,12 +234,13 @@ class PeerSolver:
     from a deterministic frontier share, frontier_per_rank > 0)."""
 
     def __init__(self, graph, mode, k, group, *, device=0, frontier_per_rank=0, expander=None,
-                 shard_factory=None, **solve_kw):
+                 shard_factory=None, detail=True, **solve_kw):
         import torch.distributed as dist
         from .shards import Shard, combine, root_frontier
         self._combine = combine
         Shard = shard_factory or Shard
         self.graph, self.mode, self.k, self.group = graph, mode, k, group
+        self.detail = detail  # gather every worker's node count (the report's worker_nodes)
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         if frontier_per_rank:
@@ -276,16 +277,49 @@ class PeerSolver:
             dist.barrier(group=self.group)  # every shard (re)initialised before any launch
             self.shard.launch()
             mine = self.shard.wait()
-            keep = ("size", "feasible", "cover", "cover_from_search", "status", "worker_nodes",
-                    "nodes_total", "device_ms", "donated", "donated_peer", "kernel_launches",
-                    "h2d_bytes", "d2h_bytes", "greedy_size")
             # (the gather is also the barrier that keeps every kernel done before any reset)
-            parts = [None] * self.world
-            dist.all_gather_object(parts, {x: mine.get(x, 0) for x in keep}, group=self.group)
+            parts = self._gather(mine)
         out = self._combine(self.graph, self.mode, self.frontier, parts,
                             (time.perf_counter() - t0) * 1e3)
         out["exchange"] = "peer"
         return out
+
+    _SCALARS = ("nodes_total", "feasible", "size", "cover_from_search", "donated",
+                "donated_peer", "kernel_launches", "h2d_bytes", "d2h_bytes", "greedy_size")
+    _STATUS = ("complete", "timeout", "budget")
+
+    def _gather(self, mine):
+        """Every rank's part: the scalars in one small tensor all-gather; covers (only when a
+        rank has one to offer) and per-worker node counts (detail) as pickled objects."""
+        import torch
+        import torch.distributed as dist
+        v = [int(mine.get(x, 0)) for x in self._SCALARS]
+        v += [self._STATUS.index(mine["status"]) if mine["status"] in self._STATUS else 0,
+              int(round(mine["device_ms"] * 1e6))]
+        t = torch.tensor(v, dtype=torch.int64)
+        got = [torch.zeros_like(t) for _ in range(self.world)]
+        dist.all_gather(got, t, group=self.group)
+        parts = []
+        for g in got:
+            g = g.tolist()
+            d = dict(zip(self._SCALARS, g))
+            d["feasible"] = bool(d["feasible"])
+            d["cover_from_search"] = bool(d["cover_from_search"])
+            d["status"] = self._STATUS[g[len(self._SCALARS)]]
+            d["device_ms"] = g[len(self._SCALARS) + 1] / 1e6
+            d["cover"], d["worker_nodes"] = [], []
+            parts.append(d)
+        need_cover = any(p["feasible"] if self.mode == "pvc" else p["cover_from_search"]
+                         for p in parts)
+        if need_cover or self.detail:
+            extra = [None] * self.world
+            dist.all_gather_object(
+                extra, dict(cover=mine["cover"] if need_cover else [],
+                            worker_nodes=mine["worker_nodes"] if self.detail else []),
+                group=self.group)
+            for p, e in zip(parts, extra):
+                p.update(e)
+        return parts
 
     def close(self):
         if self.shard is not None:
