@@ -1444,7 +1444,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             if (__shfl_sync(FULL, stop, 0)) break;
         }
 
-        if ((compact ? y.cc : x.cc) == DEAD_NODE) {  // a doomed child's marker: visited, pruned
+        // a doomed child's marker: visited, pruned (markers exist only in the one-worker
+        // strategies; the hybrid kernel never reads the wide node's local-memory copy here)
+        if (seq_mode_ && (compact ? y.cc : x.cc) == DEAD_NODE) {
             ++st.dooms;
             have = false;
             continue;
