@@ -252,9 +252,13 @@ constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
 constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1;
 
 #ifndef VCG_POLL_EVERY
-#define VCG_POLL_EVERY 8  // nodes between reads of the control line (power of two)
+#define VCG_POLL_EVERY 32  // nodes between reads of the control line (power of two; C5: 4 → 12.3 ms,
+                           // 8 → 10.1, 16 → 9.4, 32 → 9.0, 64 → 9.4)
 #endif
 constexpr uint32_t kPoll = VCG_POLL_EVERY;
+#ifndef VCG_POLL_EVERY_MULTI
+#define VCG_POLL_EVERY_MULTI 8  // linked shards poll more often: the poll also probes a peer
+#endif
 #ifndef VCG_WIDE_SMEM
 #define VCG_WIDE_SMEM 1   // wide degrees in shared memory (fewer registers) instead of registers
 #endif
@@ -1156,7 +1160,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
     int B = bound_of(a.pvc, a.k, best);  // prune once |S| > B
-    uint32_t qsize = 0, polls = kPoll - 1;  // (the first node polls)
+    constexpr uint32_t kPollK = MULTI ? VCG_POLL_EVERY_MULTI : kPoll;
+    uint32_t qsize = 0, polls = kPollK - 1;  // (the first node polls)
     bool poll = false;
     uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
     uint32_t hw = 0;             // worklist size
@@ -1399,7 +1404,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         // every kPoll nodes; in between the warp uses the last bound / queue size it saw (a
         // stale bound only prunes less; the queue size only steers donation). The read is
         // issued here and consumed after the reduction.
-        poll = (++polls & (kPoll - 1)) == 0;
+        poll = (++polls & (kPollK - 1)) == 0;
         if (poll && lane == 0) {
             h = ld_volatile_v2(ctl);
             hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
