@@ -156,6 +156,13 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps) {
                          : base + warps * (size_t)W * 32 * 4;
 }
 
+#ifndef VCG_BACKOFF_CAP_NS
+#define VCG_BACKOFF_CAP_NS 2000  // idle workers' exponential back-off cap
+#endif
+#ifndef VCG_FLUSH_EVERY
+#define VCG_FLUSH_EVERY 64  // visits between a worker's node-counter flushes / limit checks
+#endif
+
 uint32_t pick_w(uint32_t n) {
     if (n <= 128) return 4;
     if (n <= 256) return 8;
@@ -468,12 +475,12 @@ struct DenseRun {
         a.node_budget = s.node_budget;
         a.timeout_ns = s.timeout_s >= 0 ? (unsigned long long)(s.timeout_s * 1e9) : 0ull;
         if (s.timeout_s >= 0 && a.timeout_ns == 0) a.timeout_ns = 1;
-        a.flush_every = 64;
+        a.flush_every = VCG_FLUSH_EVERY;
         if (s.node_budget)
             a.flush_every = std::max<uint64_t>(1, std::min<uint64_t>(64, s.node_budget / (4ull * workers)));
         // idle back-off: exponential from 32 ns, capped at backoff_us (at most 2 us on the device —
         // a polling warp costs one L2 read, an over-sleeping one leaves queued work unclaimed)
-        a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), 2000);
+        a.backoff_ns = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(s.backoff_us * 1000, 64), VCG_BACKOFF_CAP_NS);
         a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
         a.donate_oldest = s.donate_oldest ? 1 : 0;
         a.compact = s.engine == 3 ? 0 : 1;
