@@ -40,29 +40,53 @@ constexpr unsigned long long ONE_PENDING = 1ull << 32;
 
 // ------------------------------------------------------------------ device-global state
 
+#ifndef VCG_SPLIT_TICKETS
+#define VCG_SPLIT_TICKETS 1
+#endif
+#ifndef VCG_SPLIT_WORK
+#define VCG_SPLIT_WORK 0
+#endif
 struct Ctl {
     // line 0: read by every worker once per node (one vector load + one scalar load)
     uint32_t best;    // MVC bound (atomicMin); PVC: k
     uint32_t cancel;  // 1 = stop: PVC found, timeout, budget, host request
     uint32_t found;   // PVC: a cover of size <= k was recorded
     uint32_t pad0;
+#if !VCG_SPLIT_WORK
     // (pending << 32) | size: pending = queued items + active workers (termination at 0);
     // size = queued items + in-flight enqueue reservations (threshold gate, capacity)
     unsigned long long work;
     unsigned long long pad1;
     uint32_t pad2[24];
-    // line 1: ring tickets (per-slot sequence numbers publish / free each slot)
-    unsigned long long head, tail;
+#else
+    uint32_t pad2[28];
+    // line 0b: the packed worklist word on its own line (its atomics do not contend with the
+    // reads of the bound / cancel words)
+    unsigned long long work;
+    uint32_t pad7[30];
+#endif
+    // line 1: the consumers' ring ticket (per-slot sequence numbers publish / free each slot)
+    unsigned long long head;
     // shard 0 only (multi-shard solves): number of shards whose `pending` is non-zero; the
     // whole solve is done when it reaches zero
     uint32_t gactive;
-    uint32_t pad3[27];
-    // line 2: results
+    uint32_t pad3[29];
+#if VCG_SPLIT_TICKETS
+    // line 2: the producers' ticket, on its own line (producers and consumers do not contend
+    // on one L2 line)
+    unsigned long long tail;
+    uint32_t pad5[30];
+#endif
+    // results
     unsigned long long nodes_total, best_owner;
     int32_t status;
     uint32_t pad4[27];
+#if !VCG_SPLIT_TICKETS
+    unsigned long long tail;
+    uint32_t pad6[30];
+#endif
 };
-static_assert(sizeof(Ctl) == 384, "Ctl layout");
+static_assert(sizeof(Ctl) == (VCG_SPLIT_WORK ? 640 : 512), "Ctl layout");
 
 // A peer shard's exchange memory (another GPU over NVLink P2P / CUDA IPC, or another shard on
 // this device): its control block, ring slots and slot sequence numbers.
