@@ -1184,7 +1184,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
     int B = bound_of(a.pvc, a.k, best);  // prune once |S| > B
-    constexpr uint32_t kPollK = MULTI ? VCG_POLL_EVERY_MULTI : kPoll;
+    // (small graphs, W <= 8: short trees whose time is latency — bound and cancel news must
+    // travel fast, so they keep polling every 8 nodes)
+    constexpr uint32_t kPollK = MULTI ? VCG_POLL_EVERY_MULTI : (W <= 8 ? 8u : kPoll);
     uint32_t qsize = 0, polls = kPollK - 1;  // (the first node polls)
     bool poll = false;
     uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
