@@ -1186,7 +1186,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     int B = bound_of(a.pvc, a.k, best);  // prune once |S| > B
     // (small graphs, W <= 8: short trees whose time is latency — bound and cancel news must
     // travel fast, so they keep polling every 8 nodes)
-    constexpr uint32_t kPollK = MULTI ? VCG_POLL_EVERY_MULTI : (W <= 8 ? 8u : kPoll);
+    constexpr uint32_t kPollK = W <= 8 ? 8u : kPoll;
+    bool probe_now = false;  // linked shards: probe a peer every VCG_POLL_EVERY_MULTI nodes
     uint32_t qsize = 0, polls = kPollK - 1;  // (the first node polls)
     bool poll = false;
     uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
@@ -1220,8 +1221,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 B = bound_of(0, 0, best);
             }
             qsize = __shfl_sync(FULL, hw, 0);
-            if (multi) starve = __shfl_sync(FULL, hp, 0);
         }
+        if (probe_now) starve = __shfl_sync(FULL, hp, 0);
         const bool prune = n.doom || prune_at(B, n.cc, n.edges);
         st.dooms += n.doom;
         if (prune) return ACT_POP;
@@ -1431,10 +1432,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         // stale bound only prunes less; the queue size only steers donation). The read is
         // issued here and consumed after the reduction.
         poll = (++polls & (kPollK - 1)) == 0;
+        probe_now = multi && (polls & (VCG_POLL_EVERY_MULTI - 1)) == 0;
         if (poll && lane == 0) {
             h = ld_volatile_v2(ctl);
             hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
-            if (multi) {
+        }
+        if (probe_now && lane == 0) {
+            {
                 // One peer per poll, round robin: is it below its donation threshold? The read
                 // crosses NVLink, so it is consumed one poll later (it has long arrived): the
                 // verdict on the previous probe's peer now, the next peer's read in flight.
