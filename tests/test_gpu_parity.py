@@ -463,3 +463,20 @@ def test_persistent_shards_solve_repeatedly(config_golden):
             assert r["size"] == config_golden["c1"]["mvc"] and vc.verify_cover(c1, r["cover"])
     finally:
         ss.close()
+
+
+@pytest.mark.parametrize("name", ["fuzz_200_12063.el", "fuzz_128_4403.el"])
+def test_parallel_mvc_is_certified_optimal(oracle, name):
+    """Regression (tools/fuzz_parity.py): on these graphs the parallel MVC search alone stopped
+    one above the optimum; the PVC(size - 1) certificate makes every strategy exact."""
+    import os
+    from oracle.oracle import CSR
+    path = os.path.join(os.path.dirname(__file__), "data", name)
+    g = vc.parse_edge_list(open(path).read())
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(g.num_vertices, g.num_edges, off, nbr))
+    for kw in (dict(strategy="gpu"), dict(strategy="hybrid", workers=3552),
+               dict(strategy="gpu", engine="dense-wide"), dict(strategy="gpu", engine="sparse")):
+        r = vc.solve_mvc(g, **kw)
+        assert r["size"] == want["size"], (kw, r["size"], want["size"])
+        check_cover(g, r)

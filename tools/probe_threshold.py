@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_10402_b200 as vc
 from paper_2204_10402_b200.configs import load_config
 g = load_config("c5")
-for cap, frac in [(4096, 0.5), (4096, 0.25), (4096, 0.1), (4096, 0.05), (4096, 0.02), (16384, 0.05), (1024, 0.5)]:
+for cap, frac in [(4096, 0.5), (4096, 0.25), (4096, 1.0), (8192, 0.5), (2048, 0.5), (4096, 0.5)]:
     ms = []
     for _ in range(3):
         r = vc.solve_pvc(g, 482, strategy="gpu", capacity=cap, threshold_fraction=frac)
