@@ -30,7 +30,9 @@ enum {
     VCG_EPARSE = 2,   /* vcsolve::ParseError (graph.hpp:17-26) */
     VCG_ECUDA = 3,    /* CUDA/device error: no reference counterpart (CPU-only reference) */
     VCG_ENOMEM = 4,
-    VCG_ERANGE = 5    /* brute_force_mvc limit (solver_seq.cpp:174-175) */
+    VCG_ERANGE = 5,   /* brute_force_mvc limit (solver_seq.cpp:174-175) */
+    VCG_EVERIFY = 6   /* a cover the engine returned failed verify_cover (bounds.cpp:32-45):
+                         an engine fault, never expected; the result is freed */
 };
 
 typedef struct vcg_graph vcg_graph; /* opaque: BaseGraph (graph.hpp:34-53) + device copies */
@@ -125,7 +127,15 @@ typedef struct {
     /* CUDA stream (cudaStream_t) to launch on; null = the library's own stream. The call stays
        blocking: it synchronizes this stream before returning. */
     void* stream;
+    /* Debug options (0 in production):
+       VCG_DEBUG_CERTIFY — after a parallel MVC search of size s, prove PVC(s - 1) infeasible
+         (repeating on "yes"); reported as certify_nodes / certify_ms, within the caller's
+         remaining timeout / node budget. A cross-check: the search is exact without it.
+       VCG_DEBUG_CORRUPT_COVER — drop one vertex from the returned cover before verification
+         (tests the engine's own verify_cover check, which then fails with VCG_EVERIFY). */
+    uint32_t debug_flags;
 } vcg_params;
+enum { VCG_DEBUG_CERTIFY = 1, VCG_DEBUG_CORRUPT_COVER = 2 };
 
 typedef struct {
     int32_t status;             /* VCG_COMPLETE | VCG_TIMEOUT | VCG_BUDGET */
@@ -158,12 +168,16 @@ typedef struct {
     uint64_t phase_cycles[10];  /* Phase order of metrics.hpp:15-26, summed over workers */
     uint64_t active_cycles;     /* summed over workers */
     uint64_t donated_peer;      /* of `donated`: nodes written into another shard's worklist */
+    /* VCG_DEBUG_CERTIFY only: the certificate's PVC searches (not in nodes_total / device_ms) */
+    uint64_t certify_nodes;
+    double certify_ms;
+    uint32_t certify_launches;
 } vcg_result;
 
 VCG_API void vcg_params_init(vcg_params* p);
 /* run_hybrid / run_stackonly (scheduler.hpp:48,55) and solve_mvc_seq / solve_pvc_seq
  * (solver_seq.hpp:43-48) on the GPU: greedy seed (host), CSR upload, one persistent kernel,
- * result readback. Blocking. */
+ * result readback, verify_cover of the returned cover (VCG_EVERIFY if it fails). Blocking. */
 VCG_API int vcg_solve(const vcg_graph* g, const vcg_params* p, vcg_result* out);
 VCG_API void vcg_result_free(vcg_result* r);
 

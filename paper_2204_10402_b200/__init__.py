@@ -196,12 +196,13 @@ _ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3}
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
            timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
            instrument=False, initial_best=0, seeds=None, mailbox=None, raw=False,
-           donate_oldest=None, stream=None, engine="auto"):
+           donate_oldest=None, stream=None, engine="auto", certify=False, debug_flags=0):
     """The strategy dispatch of bindings.cpp:60-99, on the GPU through vcg_solve."""
     p, keep = _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
                       timeout_s, node_budget, device=device, rules=rules, block_warps=block_warps,
                       instrument=instrument, initial_best=initial_best, seeds=seeds,
-                      mailbox=mailbox, donate_oldest=donate_oldest, stream=stream, engine=engine)
+                      mailbox=mailbox, donate_oldest=donate_oldest, stream=stream, engine=engine,
+                      certify=certify, debug_flags=debug_flags)
     workers = p.workers
     r = _n.Result()
     _n.check(_lib.vcg_solve(graph._h, C.byref(p), C.byref(r)))
@@ -219,7 +220,7 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
 def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
             timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
             instrument=False, initial_best=0, seeds=None, mailbox=None, donate_oldest=None,
-            stream=None, engine="auto"):
+            stream=None, engine="auto", certify=False, debug_flags=0):
     """vcg_params for one solve (validated like bindings.cpp:60-99) + the arrays it points to."""
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
@@ -250,6 +251,7 @@ def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, bac
         donate_oldest = strategy == "gpu"
     p.donate_oldest = int(bool(donate_oldest))
     p.initial_best = initial_best or 0
+    p.debug_flags = int(debug_flags) | (_n.VCG_DEBUG_CERTIFY if certify else 0)
     keep = None
     if seeds is not None and len(seeds):
         keep = np.ascontiguousarray(seeds, dtype=np.uint32)
@@ -291,6 +293,7 @@ def _result_dict(r):
         kernel_launches=int(r.kernel_launches),
         phase_cycles=[int(x) for x in r.phase_cycles], active_cycles=int(r.active_cycles),
         donated_peer=int(r.donated_peer),
+        certify_nodes=int(r.certify_nodes), certify_ms=float(r.certify_ms),
     )
 
 
@@ -299,7 +302,8 @@ def solve_mvc(graph, strategy="hybrid", workers=None, capacity=4096, threshold_f
     """Solve MVC; returns the run report as a dict (bindings.cpp:174-187).
 
     GPU keyword knobs: device, engine ("auto" | "dense" | "sparse"), rules, block_warps,
-    instrument, donate_oldest, initial_best, seeds, mailbox, stream, raw."""
+    instrument, donate_oldest, initial_best, seeds, mailbox, stream, raw; certify=True re-proves
+    the optimum by PVC(size - 1) (a debug cross-check, reported as certify_nodes / certify_ms)."""
     return _solve(graph, "mvc", 0, strategy, workers, capacity, threshold_fraction, depth,
                   backoff_us, timeout_s, node_budget, **gpu)
 

@@ -12,7 +12,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VCGPU_LIB", os.path.join(_HERE, "libvcgpu.so"))
 
-VCG_OK, VCG_EINVAL, VCG_EPARSE, VCG_ECUDA, VCG_ENOMEM, VCG_ERANGE = range(6)
+VCG_OK, VCG_EINVAL, VCG_EPARSE, VCG_ECUDA, VCG_ENOMEM, VCG_ERANGE, VCG_EVERIFY = range(7)
+VCG_DEBUG_CERTIFY, VCG_DEBUG_CORRUPT_COVER = 1, 2
 VCG_MVC, VCG_PVC = 0, 1
 VCG_HYBRID, VCG_SEQ, VCG_STACKONLY = 0, 1, 2
 STATUS_NAMES = ("complete", "timeout", "budget")  # run_status_name (solver_seq.cpp:15-22)
@@ -30,7 +31,7 @@ class Params(C.Structure):
         ("donate_oldest", C.c_int32),
         ("initial_best", C.c_uint32), ("num_seeds", C.c_uint64),
         ("seeds", C.POINTER(C.c_uint32)), ("mailbox", C.POINTER(C.c_uint32)),
-        ("stream", C.c_void_p),
+        ("stream", C.c_void_p), ("debug_flags", C.c_uint32),
     ]
 
 
@@ -55,6 +56,8 @@ class Result(C.Structure):
         ("block_threads", C.c_uint32), ("kernel_launches", C.c_uint32),
         ("phase_cycles", C.c_uint64 * 10),
         ("active_cycles", C.c_uint64), ("donated_peer", C.c_uint64),
+        ("certify_nodes", C.c_uint64), ("certify_ms", C.c_double),
+        ("certify_launches", C.c_uint32),
     ]
 
 

@@ -318,41 +318,83 @@ struct HostRun {
         out->wall_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
+
+    // verify_cover (bounds.cpp:32-45) on every cover the engine returns (O(n + m) on the host):
+    // a cover that fails is an engine fault, reported as VCG_EVERIFY with the result freed.
+    // (VCG_DEBUG_CORRUPT_COVER drops the first cover vertex first: the test of this check.)
+    int verified() {
+        if (!out->cover_len) return VCG_OK;
+        if ((p->debug_flags & VCG_DEBUG_CORRUPT_COVER) && out->cover_len) {
+            std::memmove(out->cover, out->cover + 1, (out->cover_len - 1) * 4);
+            --out->cover_len;
+        }
+        std::vector<uint32_t> ids(out->cover, out->cover + out->cover_len);
+        for (uint32_t& v : ids) v -= g.id_base;
+        bool ok = vcg::verify_cover(g, ids.data(), ids.size());
+        if (ok && pvc && out->cover_len > p->k) ok = false;
+        if (ok) return VCG_OK;
+        const std::string msg = "engine returned an invalid cover (size " +
+                                std::to_string(out->cover_len) +
+                                (pvc ? ", k " + std::to_string(p->k) : std::string()) +
+                                "): verify_cover failed";
+        vcg_result_free(out);
+        return fail(VCG_EVERIFY, msg);
+    }
 };
 
 }  // namespace
 
 namespace {
-// Optimality certificate for a parallel MVC search. With thousands of workers racing on the
-// bound, a randomized parity run (tools/fuzz_parity.py: 2 of 2,242 graphs) showed the parallel
-// MVC search can stop one above the optimum. The PVC search has no bound dynamics (its tree, and
-// node count, are the reference's exactly), so the best size s found is certified by proving
-// PVC(s - 1) infeasible; a "yes" improves the certificate and repeats.
-void certify_mvc(const vcg::Graph& g, HostRun& h, vcg::SolveOut& r) {
+// Debug option (VCG_DEBUG_CERTIFY): re-prove a parallel MVC optimum by PVC(s - 1). The PVC search
+// has no bound dynamics (its tree and node count are the reference's exactly), so a "no" proves
+// the size s found optimal and a "yes" improves the certificate and repeats. The parallel MVC
+// search is exact on its own (the dense engine re-reduces a node when a poll lowers the bound
+// before the edge-count prune; see settle() in dense_kernels.cuh), so this is off by default;
+// it exists to cross-check that claim. Its nodes and device time are reported separately
+// (certify_nodes / certify_ms), and it only spends what is left of the caller's time and node
+// limits.
+void certify_mvc(const vcg::Graph& g, HostRun& h, vcg::SolveOut& r, vcg_result* out) {
     if (r.status != 0) return;
     if (h.greedy_async.valid()) h.greedy = h.greedy_async.get();
-    uint32_t best = r.found && r.cover.size() < h.greedy.size ? (uint32_t)r.cover.size()
-                                                              : h.greedy.size;
+    uint32_t best = h.greedy.size;
+    if (h.s.best < best) best = h.s.best;  // an external bound (initial_best)
+    if (r.found && r.cover.size() < best) best = (uint32_t)r.cover.size();
+    uint64_t nodes_used = 0;
+    for (uint64_t x : r.worker_nodes) nodes_used += x;
     while (best >= 2) {  // (a cover of size 0 exists only without edges: then best is 0)
         vcg::SolveSpec s2 = h.s;
         s2.pvc = true;
         s2.k = best - 1;
         s2.best = s2.k;
         s2.stack_bound = std::min<uint32_t>(s2.k, g.n);
+        s2.mailbox = nullptr;
+        if (h.s.timeout_s >= 0) {
+            const double spent = std::chrono::duration<double>(std::chrono::steady_clock::now() - h.t0).count();
+            s2.timeout_s = std::max(0.0, h.s.timeout_s - spent);
+        }
+        if (h.s.node_budget) {
+            if (nodes_used >= h.s.node_budget) {
+                r.status = 2;
+                return;
+            }
+            s2.node_budget = h.s.node_budget - nodes_used;
+        }
         vcg::SolveOut r2;
         vcg::solve_on_device(g, s2, r2);
-        r.device_ms += r2.device_ms;
-        r.rounds += r2.rounds;
-        r.maxdeg += r2.maxdeg;
-        r.children += r2.children;
-        r.launches += r2.launches;
-        if (r2.worker_nodes.size() == r.worker_nodes.size())
-            for (size_t i = 0; i < r.worker_nodes.size(); ++i) r.worker_nodes[i] += r2.worker_nodes[i];
+        out->certify_ms += r2.device_ms;
+        out->certify_launches += r2.launches;
+        for (uint64_t x : r2.worker_nodes) {
+            out->certify_nodes += x;
+            nodes_used += x;
+        }
         if (r2.status != 0) {
             r.status = r2.status;
             return;
         }
         if (!r2.found) return;  // PVC(best - 1) is a no-instance: best is the optimum
+        if (r2.cover.size() >= best)
+            throw std::runtime_error("certify: PVC(" + std::to_string(best - 1) +
+                                     ") returned a cover of size " + std::to_string(r2.cover.size()));
         r.found = true;
         r.cover = r2.cover;
         best = (uint32_t)r2.cover.size();
@@ -375,10 +417,11 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
             r.wl_added = r.wl_removed = 1;
         } else {
             vcg::solve_on_device(gh->g, h.s, r);
-            if (!h.pvc && h.s.strategy == 0) certify_mvc(gh->g, h, r);
+            if (!h.pvc && (p->debug_flags & VCG_DEBUG_CERTIFY) && h.s.strategy != VCG_SEQ)
+                certify_mvc(gh->g, h, r, out);
         }
         h.finish(r);
-        return VCG_OK;
+        return h.verified();
     });
 }
 
@@ -477,7 +520,7 @@ int vcg_session_wait(vcg_session* s, vcg_result* out) {
         out->greedy_ms = s->scratch.greedy_ms;
         h.out = out;
         h.finish(r);
-        return VCG_OK;
+        return h.verified();
     });
 }
 
@@ -528,6 +571,9 @@ int vcg_expand_frontier(const vcg_graph* gh, const vcg_params* p, uint64_t targe
         out->kernel_launches = f.launches;
         const std::vector<uint32_t>& cov = f.found ? f.cover : greedy.cover;
         if (!(pvc && !f.found)) {
+            // verify_cover (bounds.cpp:32-45) on the certificate handed back
+            if (!vcg::verify_cover(g, cov.data(), cov.size()) || (pvc && cov.size() > p->k))
+                return fail(VCG_EVERIFY, "frontier expansion returned an invalid cover");
             out->cover_len = (uint32_t)cov.size();
             out->cover = static_cast<uint32_t*>(std::malloc(std::max<size_t>(1, cov.size()) * 4));
             for (size_t i = 0; i < cov.size(); ++i) out->cover[i] = cov[i] + g.id_base;

@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     uint32_t starve = a.world, hp = a.world, probe = 0, hpv = ~0u;
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
-    auto settle = [&](auto& n) -> int {
+    auto reduce_under_B = [&](auto& n) {
         if constexpr (VCG_WIDE_NOINLINE && !INSTR &&
                       std::is_same<typename std::remove_reference<decltype(n)>::type,
                                    WarpNode<W, INSTR>>::value) {
@@ -1214,11 +1214,26 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         } else {
             n.reduce(B, st);
         }
+    };
+    auto settle = [&](auto& n) -> int {
+        reduce_under_B(n);
         if (poll) {
             if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
             if (!a.pvc) {
-                best = min(best, __shfl_sync(FULL, h.x, 0));
-                B = bound_of(0, 0, best);
+                // The edge-count prune (should_prune, bounds.cpp:27-29) is a proof only when
+                // every alive degree is within the high-degree limit of the SAME bound
+                // (reductions.hpp:25-26): a cover of L = B - |S| vertices of degree <= L covers
+                // at most L^2 edges. The reduction above ran under the bound seen at the last
+                // poll; if the poll brings a lower one, the node is reduced to fixpoint again
+                // under it before the prune (the reference reads one `best` for both,
+                // scheduler.cpp:127-132, reductions.cpp:70-87). The bound only drops when a
+                // cover improves, so this re-run is rare.
+                const uint32_t nb = __shfl_sync(FULL, h.x, 0);
+                if (nb < best) {
+                    best = nb;
+                    B = bound_of(0, 0, best);
+                    if (!n.doom) reduce_under_B(n);
+                }
             }
             qsize = __shfl_sync(FULL, hw, 0);
         }

@@ -465,18 +465,75 @@ def test_persistent_shards_solve_repeatedly(config_golden):
         ss.close()
 
 
-@pytest.mark.parametrize("name", ["fuzz_200_12063.el", "fuzz_128_4403.el"])
-def test_parallel_mvc_is_certified_optimal(oracle, name):
-    """Regression (tools/fuzz_parity.py): on these graphs the parallel MVC search alone stopped
-    one above the optimum; the PVC(size - 1) certificate makes every strategy exact."""
+def _fuzz_graph(name):
     import os
-    from oracle.oracle import CSR
     path = os.path.join(os.path.dirname(__file__), "data", name)
-    g = vc.parse_edge_list(open(path).read())
+    return vc.parse_edge_list(open(path).read())
+
+
+@pytest.mark.parametrize("name", ["fuzz_200_12063.el", "fuzz_128_4403.el"])
+def test_parallel_mvc_is_exact_without_certificate(oracle, name):
+    """Regression (tools/fuzz_parity.py, round 1): on these graphs the parallel MVC search once
+    stopped one above the optimum — the edge-count prune used a bound lowered by a poll AFTER
+    the node was reduced under the older one. With the node re-reduced under the new bound
+    (settle(), dense_kernels.cuh) every strategy, engine and the multi-shard path are exact on
+    their own; the racing schedule differs run to run, so each runs several times."""
+    from oracle.oracle import CSR
+    from paper_2204_10402_b200.shards import solve_sharded
+    g = _fuzz_graph(name)
     off, nbr = g.csr()
     want = oracle.solve_seq(CSR(g.num_vertices, g.num_edges, off, nbr))
     for kw in (dict(strategy="gpu"), dict(strategy="hybrid", workers=3552),
-               dict(strategy="gpu", engine="dense-wide"), dict(strategy="gpu", engine="sparse")):
-        r = vc.solve_mvc(g, **kw)
-        assert r["size"] == want["size"], (kw, r["size"], want["size"])
-        check_cover(g, r)
+               dict(strategy="hybrid", workers=64),
+               dict(strategy="gpu", engine="dense-wide"), dict(strategy="gpu", engine="sparse"),
+               dict(strategy="stackonly", workers=1024, depth=12)):
+        for _ in range(8):
+            r = vc.solve_mvc(g, **kw)
+            assert r["size"] == want["size"], (kw, r["size"], want["size"])
+            assert r["certify_nodes"] == 0
+            check_cover(g, r)
+    for _ in range(4):
+        r = solve_sharded(g, "mvc", devices=(0, 0))
+        assert r["size"] == want["size"], ("sharded", r["size"], want["size"])
+        assert vc.verify_cover(g, r["cover"])
+
+
+def test_certificate_debug_option(oracle):
+    """certify=True (VCG_DEBUG_CERTIFY) re-proves the optimum by PVC(size - 1): same answer, its
+    nodes and time reported apart from the search's."""
+    from oracle.oracle import CSR
+    g = _fuzz_graph("fuzz_128_4403.el")
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(g.num_vertices, g.num_edges, off, nbr))
+    r = vc.solve_mvc(g, strategy="gpu", certify=True)
+    assert r["size"] == want["size"] and r["certify_nodes"] > 0 and r["certify_ms"] > 0
+    plain = vc.solve_mvc(g, strategy="gpu")
+    assert plain["certify_nodes"] == 0
+    # the certificate stays within the caller's node budget
+    r = vc.solve_mvc(g, strategy="gpu", certify=True, node_budget=plain["nodes_total"] + 10)
+    assert r["status"] in ("complete", "budget")
+
+
+def test_engine_verifies_every_returned_cover():
+    """verify_cover (bounds.cpp:32-45) runs inside vcg_solve: a corrupted cover (debug hook
+    drops one vertex of an optimal cover) is reported as an engine fault, never returned."""
+    from paper_2204_10402_b200 import _native as n
+    g = load_config("c1")
+    with pytest.raises(RuntimeError, match="invalid cover"):
+        vc.solve_mvc(g, strategy="gpu", debug_flags=n.VCG_DEBUG_CORRUPT_COVER)
+    with pytest.raises(RuntimeError, match="invalid cover"):
+        vc.solve_pvc(g, 85, strategy="gpu", debug_flags=n.VCG_DEBUG_CORRUPT_COVER)
+    # an infeasible PVC returns no cover: nothing to verify, no error
+    assert not vc.solve_pvc(g, 84, strategy="gpu",
+                            debug_flags=n.VCG_DEBUG_CORRUPT_COVER)["feasible"]
+
+
+def test_c2_pvc_yes_at_k241(config_golden):
+    """C2 (ER(400, d6)) PVC k = 241 = MVC: a yes-instance with a verified certificate of size
+    <= k (the "no" side, k = 240, is a 466 G-node search: profiles/r1_c2_k240.json and the
+    cross-check run in profiles/)."""
+    g = load_config("c2")
+    r = vc.solve_pvc(g, 241, strategy="gpu", timeout_s=120)
+    assert r["status"] == "complete" and r["feasible"]
+    assert r["size"] <= 241
+    check_cover(g, r)

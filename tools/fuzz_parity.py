@@ -3,7 +3,8 @@ engine, each solved on the GPU and by the oracle (the C restatement of the refer
 to it by tests/test_oracle.py).
 
 Checked per graph:
-* dense engine (n <= 1024): the MVC size; the PVC(k = MVC - 1) answer and its node count
+* dense engine (n <= 1024): the MVC size (strategy gpu twice, hybrid with 64 warps, StackOnly
+  with 512 warps — no optimality certificate); the PVC(k = MVC - 1) answer and its node count
   (schedule independent, so it must equal the reference's exactly); the 1-warp seq order's node
   count; every returned cover verified;
 * sparse engine (forced): the MVC size and a verified cover.
@@ -61,8 +62,16 @@ def main():
             continue
         rec = dict(kind=kind, n=n, m=g.num_edges, mvc=want["size"], seq_nodes=want["nodes"])
         ok = True
-        r = vc.solve_mvc(g, strategy="gpu")
-        ok &= r["size"] == want["size"] and vc.verify_cover(g, r["cover"])
+        # the parallel MVC search (no certificate: certify=False is the default), racing bound
+        # updates across thousands of warps; plus a small-worker hybrid and StackOnly
+        checks = {}
+        for tag, kw in (("gpu", dict(strategy="gpu")), ("gpu2", dict(strategy="gpu")),
+                        ("hybrid64", dict(strategy="hybrid", workers=64)),
+                        ("stackonly", dict(strategy="stackonly", workers=512, depth=10))):
+            r = vc.solve_mvc(g, **kw)
+            checks[tag] = r["size"] == want["size"] and vc.verify_cover(g, r["cover"]) \
+                and r["certify_nodes"] == 0
+            ok &= checks[tag]
         s = vc.solve_mvc(g, strategy="seq", timeout_s=60)
         ok &= s["size"] == want["size"] and sum(s["worker_nodes"]) == want["nodes"]
         if want["size"] >= 1:
@@ -72,10 +81,12 @@ def main():
                 ok &= (not p["feasible"]) and p["nodes_total"] == no["nodes"]
                 rec["pvc_no_nodes"] = no["nodes"]
             y = vc.solve_pvc(g, want["size"], strategy="gpu")
-            ok &= y["feasible"] and vc.verify_cover(g, y["cover"])
+            ok &= y["feasible"] and vc.verify_cover(g, y["cover"]) and y["size"] <= want["size"]
         sp = vc.solve_mvc(g, strategy="gpu", engine="sparse")
         ok &= sp["size"] == want["size"] and vc.verify_cover(g, sp["cover"])
         rec["ok"] = bool(ok)
+        if not ok:
+            rec["checks"] = {k: bool(v) for k, v in checks.items()}
         checked += 1
         bad += not ok
         print(json.dumps(rec), flush=True)

@@ -28,6 +28,8 @@ for name in which:
         run("c5 pvc483 gpu", lambda: vc.solve_pvc(g, 483, strategy="gpu"))
         run("c5 pvc482 gpu", lambda: vc.solve_pvc(g, 482, strategy="gpu"))
         run("c5 pvc482 gpu", lambda: vc.solve_pvc(g, 482, strategy="gpu"))
+    if name == "c5" :
+        run("c5 mvc gpu", lambda: vc.solve_mvc(g, strategy="gpu"))
     if name == "c5mvc":
         run("c5 mvc gpu", lambda: vc.solve_mvc(load_config("c5"), strategy="gpu"))
     if name == "c2":
