@@ -32,6 +32,10 @@ WORKLOAD = ("C5: PVC k=482 (=MVC-1, no-instance) on the complement of p_hat-styl
             "G(500, a=0.25, b=0.75) seed 0")
 K_NO = 482
 C5_NODES = 21461369  # reference node count (tests/golden/configs.json)
+# Degree entries are u16 in every node record (the roofline's w = 2 bytes); in registers the
+# engine works on 32-bit words and 64-bit adjacency masks. Exact integer work either way.
+DTYPE = "u16"
+DTYPE_NOTE = "u16 degree entries in node records (roofline w=2 B); u32/u64 bit-mask arithmetic"
 
 
 def parse():
@@ -56,9 +60,20 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def csr_of(graph):
-    off, nbr = graph.csr()
-    return off, nbr
+def config_text(name):
+    """The frozen config graph's DIMACS text, read straight from data/configs (the reference arm
+    must not import the product package)."""
+    import gzip
+    with gzip.open(os.path.join(ROOT, "data", "configs", name + ".clq.gz"), "rt") as f:
+        return f.read()
+
+
+def bench_config(n, m, world):
+    """The workload dict, identical in both arms."""
+    return {"workload": WORKLOAD, "n": n, "m": m, "k": K_NO, "nodes_per_step": C5_NODES,
+            "l2": "flushed between timed steps (256 MB memset)",
+            "parallelism": "1 GPU" if world == 1 else
+            f"{world} GPUs, one shard each, worklists linked over NVLink P2P (CUDA IPC)"}
 
 
 # ---------------------------------------------------------------- clocks during the timed region
@@ -154,8 +169,7 @@ def ncu_traffic():
 def reference_line(args, rank, world):
     if rank != 0:
         return
-    from oracle.oracle import CSR, Reference
-    from paper_2204_10402_b200.configs import config_text
+    from oracle.oracle import Reference
     ref = Reference()
     g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
     cores = os.cpu_count() or 1
@@ -175,9 +189,9 @@ def reference_line(args, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
-        "config": {"workload": WORKLOAD, "n": g.n, "m": g.m, "k": K_NO, "threads": cores},
+        "config": bench_config(g.n, g.m, world),
         "time_to_solution_s_est": C5_NODES / value,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
@@ -189,7 +203,6 @@ def cpu_baseline(sample_s):
     """The reference on the box's host cores, bounded sample (rank 0, N=1 only)."""
     try:
         from oracle.oracle import Reference
-        from paper_2204_10402_b200.configs import config_text
         ref = Reference()
     except OSError as e:
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
@@ -366,13 +379,11 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
         "time_to_solution_s": elapsed_ms / 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
+        "dtype_note": DTYPE_NOTE,
         "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
-        "config": {"workload": WORKLOAD, "n": n, "m": m, "k": K_NO,
-                   "nodes_per_step": nodes_per_step, "strategy": "gpu",
-                   "l2": "flushed between timed steps (256 MB memset)",
-                   "parallelism": "1 GPU" if world == 1 else
-                   f"{world} GPUs, one shard each, worklists linked over NVLink P2P (CUDA IPC)"},
+        "config": bench_config(n, m, world),
+        "nodes_per_step": nodes_per_step, "strategy": "gpu",
         "clocks": clk,
         "gpu_launches": sum(r["kernel_launches"] for r in results),
     }

@@ -118,8 +118,9 @@ static int reduce(node_t* x, uint32_t k) {
 
 static node_t stack_[4096];
 static uint32_t depth_[4096];
-static uint32_t pw_[4096], pc_[4096];  /* wide / compact visits on the root path */
-static uint64_t best_w, best_c, best_cost;
+static uint32_t pw_[4096], pc_[4096], pb_[4096][3];  /* wide / compact visits on the root path;
+                                                      wide by alive band 65-128, 129-256, >256 */
+static uint64_t best_w, best_c, best_cost, best_b[3];
 static uint64_t wide_depth_h[1024];
 static uint32_t alive_count(const void* xv) {
     const node_t* x = xv;
@@ -164,7 +165,7 @@ int main(int argc, char** argv) {
     depth_[0] = 0;
     while (sp > 0) {
         uint32_t dep = depth_[--sp];
-        uint32_t pw = pw_[sp], pc = pc_[sp];
+        uint32_t pw = pw_[sp], pc = pc_[sp], pb[3] = {pb_[sp][0], pb_[sp][1], pb_[sp][2]};
         x = stack_[sp];
         for (;;) {
             st_nodes++;
@@ -174,8 +175,9 @@ int main(int argc, char** argv) {
                 st_alive_visit[a >= 512 ? 16 : a / 32]++;
                 if (a > 64) wide_depth_h[dep < 1023 ? dep : 1023]++;
                 if (a > 64) pw++; else pc++;
+                if (a > 64) pb[a > 256 ? 2 : a > 128 ? 1 : 0]++;
                 uint64_t cost = 8ull * pw + pc;
-                if (cost > best_cost) { best_cost = cost; best_w = pw; best_c = pc; }
+                if (cost > best_cost) { best_cost = cost; best_w = pw; best_c = pc; memcpy(best_b, (uint64_t[3]){pb[0], pb[1], pb[2]}, sizeof best_b); }
             }
             if (reduce(&x, k)) break;
             if (x.edges == 0) { printf("cover found (yes-instance)\n"); return 0; }
@@ -238,6 +240,7 @@ int main(int argc, char** argv) {
                 depth_[sp] = dep + 1;
                 pw_[sp] = pw;
                 pc_[sp] = pc;
+                memcpy(pb_[sp], pb, sizeof pb);
                 stack_[sp++] = ch;
                 st_stored++;
             }
@@ -262,7 +265,7 @@ done:
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_visit[i]);
     printf("\nalive at branch (x32):");
     for (int i = 0; i <= 16; ++i) printf(" %d:%lu", i, st_alive_branch_h[i]);
-    printf("\ncritical path (8 x wide + compact): %lu wide + %lu compact visits", best_w, best_c);
+    printf("\ncritical path (8 x wide + compact): %lu wide + %lu compact visits (wide by alive: 65-128 %lu, 129-256 %lu, >256 %lu)", best_w, best_c, best_b[0], best_b[1], best_b[2]);
     printf("\nwide visits by depth:");
     for (int i = 0; i < 1024; ++i) if (wide_depth_h[i]) printf(" %d:%lu", i, wide_depth_h[i]);
     printf("\ndead words hist:");
