@@ -93,8 +93,11 @@ typedef struct {
     int32_t mode;               /* VCG_MVC | VCG_PVC */
     uint32_t k;                 /* PVC parameter, >= 1 */
     int32_t strategy;           /* VCG_HYBRID | VCG_SEQ | VCG_STACKONLY */
-    uint32_t workers;           /* worker count (one worker = one warp or one block);
-                                   0 = fill every SM of the device */
+    uint32_t workers;           /* the reference's num_workers. VCG_HYBRID: the device is
+                                   always filled (see device_workers) and the per-worker report
+                                   is folded into this many entries (device worker i counts for
+                                   entry i % workers; 0 = one entry per device worker).
+                                   VCG_STACKONLY: device workers (one warp or one block each). */
     uint64_t capacity;          /* worklist capacity (entries) */
     double threshold_fraction;  /* (0, 1] → threshold = clamp(llround(f*cap), 1, cap) */
     uint32_t depth;             /* StackOnly sub-tree depth in [1, 30] */
@@ -107,12 +110,15 @@ typedef struct {
     uint32_t block_warps;       /* warps per CTA, 0 = auto */
     int32_t engine;             /* 0 auto, 1 dense (n <= 1024, warp per node),
                                    2 sparse (any n, CTA per node),
-                                   3 dense without compact renumbering (every node in the wide
-                                     32*W-slot layout; for A/B tests) */
+                                   3 dense without renumbering (every node in the wide 32*W-slot
+                                     layout; for A/B tests),
+                                   4 dense without the mid (<= 128 alive, per-warp frame) layout
+                                     (wide and compact only; for A/B tests) */
     int32_t instrument;         /* 1: per-worker phase cycle counters */
-    int32_t donate_oldest;      /* 1: when donating, hand over the OLDEST stacked node (largest
-                                   expected sub-tree) and stack the new child; 0: donate the new
-                                   remove-N(v) child as the reference does (scheduler.cpp:191-199) */
+    int32_t donate_oldest;      /* 1 (vcg_params_init's default): when donating, hand over the
+                                   OLDEST stacked node (largest expected sub-tree) and stack the
+                                   new child; 0: donate the new remove-N(v) child as the reference
+                                   does (scheduler.cpp:191-199) */
     uint32_t initial_best;      /* MVC: external upper bound (e.g. from another rank),
                                    0 = none; never replaces the greedy certificate */
     /* Seeding (multi-GPU frontier shares): when num_seeds > 0, the worklist starts with these
@@ -134,6 +140,10 @@ typedef struct {
        VCG_DEBUG_CORRUPT_COVER — drop one vertex from the returned cover before verification
          (tests the engine's own verify_cover check, which then fails with VCG_EVERIFY). */
     uint32_t debug_flags;
+    /* Device workers (warps of the dense engine, CTAs of the sparse engine) to run. 0 = every
+       SM filled (VCG_HYBRID) / `workers` (VCG_STACKONLY). Set it to run a fixed number, e.g.
+       to give several shards on one device their share. */
+    uint32_t device_workers;
 } vcg_params;
 enum { VCG_DEBUG_CERTIFY = 1, VCG_DEBUG_CORRUPT_COVER = 2 };
 

@@ -190,19 +190,20 @@ def load_graph(path, fmt=None, complement_input=False) -> BaseGraph:
 _STRATEGIES = {"hybrid": _n.VCG_HYBRID, "gpu": _n.VCG_HYBRID, "seq": _n.VCG_SEQ,
                "stackonly": _n.VCG_STACKONLY}
 _RULES = {"reference": 0, "parallel": 1}
-_ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3}
+_ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3, "dense-nomid": 4}
 
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
            timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
            instrument=False, initial_best=0, seeds=None, mailbox=None, raw=False,
-           donate_oldest=None, stream=None, engine="auto", certify=False, debug_flags=0):
+           donate_oldest=None, stream=None, engine="auto", certify=False, debug_flags=0,
+           device_workers=None):
     """The strategy dispatch of bindings.cpp:60-99, on the GPU through vcg_solve."""
     p, keep = _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
                       timeout_s, node_budget, device=device, rules=rules, block_warps=block_warps,
                       instrument=instrument, initial_best=initial_best, seeds=seeds,
                       mailbox=mailbox, donate_oldest=donate_oldest, stream=stream, engine=engine,
-                      certify=certify, debug_flags=debug_flags)
+                      certify=certify, debug_flags=debug_flags, device_workers=device_workers)
     workers = p.workers
     r = _n.Result()
     _n.check(_lib.vcg_solve(graph._h, C.byref(p), C.byref(r)))
@@ -220,8 +221,13 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
 def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,
             timeout_s, node_budget, *, device=0, rules="reference", block_warps=0,
             instrument=False, initial_best=0, seeds=None, mailbox=None, donate_oldest=None,
-            stream=None, engine="auto", certify=False, debug_flags=0):
-    """vcg_params for one solve (validated like bindings.cpp:60-99) + the arrays it points to."""
+            stream=None, engine="auto", certify=False, debug_flags=0, device_workers=None):
+    """vcg_params for one solve (validated like bindings.cpp:60-99) + the arrays it points to.
+
+    Workers: "hybrid" keeps the reference's meaning of ``workers`` (its report has that many
+    entries) but always fills the device — its device workers are folded into the report —
+    unless ``device_workers`` fixes the warp / CTA count. "gpu": ``workers`` = device workers
+    (0 = fill the device), one report entry each. "stackonly": ``workers`` device workers."""
     if strategy not in _STRATEGIES:
         raise ValueError(f"unknown strategy: {strategy}")  # bindings.cpp:92
     if engine not in _ENGINES:
@@ -235,7 +241,12 @@ def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, bac
     p.mode = _n.VCG_PVC if mode == "pvc" else _n.VCG_MVC
     p.k = k
     p.strategy = _STRATEGIES[strategy]
-    p.workers = workers
+    if device_workers is not None and device_workers < 1:
+        raise ValueError("device_workers must be >= 1")
+    if strategy == "gpu":
+        p.workers, p.device_workers = 0, workers
+    else:
+        p.workers, p.device_workers = workers, device_workers or 0
     p.capacity = capacity
     p.threshold_fraction = threshold_fraction
     p.depth = depth
@@ -247,8 +258,10 @@ def _params(mode, k, strategy, workers, capacity, threshold_fraction, depth, bac
     p.block_warps = block_warps
     p.engine = _ENGINES[engine]
     p.instrument = int(bool(instrument))
-    if donate_oldest is None:  # the tuned GPU policy for "gpu"; the reference policy for "hybrid"
-        donate_oldest = strategy == "gpu"
+    if donate_oldest is None:
+        # the tuned policy on a filled device; the reference's (donate the new child) when
+        # hybrid runs a fixed, small number of device workers
+        donate_oldest = not (strategy == "hybrid" and device_workers)
     p.donate_oldest = int(bool(donate_oldest))
     p.initial_best = initial_best or 0
     p.debug_flags = int(debug_flags) | (_n.VCG_DEBUG_CERTIFY if certify else 0)
@@ -301,7 +314,7 @@ def solve_mvc(graph, strategy="hybrid", workers=None, capacity=4096, threshold_f
               depth=8, backoff_us=50, timeout_s=None, node_budget=None, **gpu):
     """Solve MVC; returns the run report as a dict (bindings.cpp:174-187).
 
-    GPU keyword knobs: device, engine ("auto" | "dense" | "sparse"), rules, block_warps,
+    GPU keyword knobs: device, device_workers, engine ("auto" | "dense" | "sparse"), rules, block_warps,
     instrument, donate_oldest, initial_best, seeds, mailbox, stream, raw; certify=True re-proves
     the optimum by PVC(size - 1) (a debug cross-check, reported as certify_nodes / certify_ms)."""
     return _solve(graph, "mvc", 0, strategy, workers, capacity, threshold_fraction, depth,

@@ -32,6 +32,7 @@ class Params(C.Structure):
         ("initial_best", C.c_uint32), ("num_seeds", C.c_uint64),
         ("seeds", C.POINTER(C.c_uint32)), ("mailbox", C.POINTER(C.c_uint32)),
         ("stream", C.c_void_p), ("debug_flags", C.c_uint32),
+        ("device_workers", C.c_uint32),
     ]
 
 

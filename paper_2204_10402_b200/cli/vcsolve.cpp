@@ -401,7 +401,10 @@ RunReport run_one(const vcg_graph* g, const SolveOptions& o) {
     p.k = o.mode == "pvc" ? *o.k : 0;
     p.strategy = o.strategy == "seq" ? VCG_SEQ : o.strategy == "stackonly" ? VCG_STACKONLY
                                                                            : VCG_HYBRID;
-    p.workers = o.strategy == "seq" ? 1 : workers;
+    // hybrid: the reference's worker count shapes the report, the device is filled; gpu: the
+    // count is device workers (0 = fill the device); stackonly: device workers
+    p.workers = o.strategy == "seq" ? 1 : o.strategy == "gpu" ? 0 : workers;
+    if (o.strategy == "gpu") p.device_workers = workers;
     p.capacity = o.capacity;
     p.threshold_fraction = o.threshold_fraction;
     p.depth = o.depth;
@@ -409,7 +412,7 @@ RunReport run_one(const vcg_graph* g, const SolveOptions& o) {
     p.timeout_s = o.timeout_s ? *o.timeout_s : -1.0;
     p.node_budget = o.node_budget ? *o.node_budget : 0;
     p.device = o.device;
-    p.donate_oldest = o.strategy == "gpu";  // the tuned device policy; hybrid keeps the reference's
+    // (donate_oldest: vcg_params_init's default, the tuned policy of a filled device)
     vcg_result res;
     std::memset(&res, 0, sizeof res);
     check(vcg_solve(g, &p, &res));
@@ -643,7 +646,8 @@ const char* kUsage =
     "  --mode mvc|pvc              Problem variant\n"
     "  --k K                       Cover size bound for pvc\n"
     "  --strategy seq|stackonly|hybrid|gpu|oracle\n"
-    "  --workers N                 Worker count (warps on the device; gpu: 0 = fill device)\n"
+    "  --workers N                 Worker count (hybrid: report entries, the device is always\n"
+    "                              filled; gpu/stackonly: warps on the device, gpu 0 = fill)\n"
     "  --worklist-capacity C       Hybrid worklist capacity\n"
     "  --threshold-fraction F      Hybrid donation threshold as a fraction of capacity\n"
     "  --depth D                   StackOnly sub-tree starting depth (1..30)\n"

@@ -176,6 +176,7 @@ void vcg_params_init(vcg_params* p) {
     p->backoff_us = 50;             // bindings.cpp:178
     p->timeout_s = -1.0;
     p->rules = VCG_RULES_REFERENCE;
+    p->donate_oldest = 1;
 }
 
 namespace {
@@ -224,7 +225,10 @@ struct HostRun {
         s.pvc = pvc;
         s.k = p->k;
         s.strategy = p->strategy;
-        s.workers = p->workers;
+        // hybrid fills the device unless device_workers says otherwise; the reference's
+        // num_workers only shapes the report (finish folds the device workers into it)
+        s.workers = p->device_workers ? p->device_workers
+                                      : (p->strategy == VCG_HYBRID ? 0u : p->workers);
         s.capacity = p->capacity;
         // worklist_threshold (scheduler.cpp:14-18)
         long long t = std::llround(p->threshold_fraction * double(p->capacity));
@@ -280,13 +284,20 @@ struct HostRun {
         }
         out->cover_len = cov ? (uint32_t)cov->size() : 0;
         out->status = r.status;
-        out->num_workers = (uint32_t)r.worker_nodes.size();
-        out->worker_nodes = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, r.worker_nodes.size()) * 8));
-        out->worker_stack_high_water =
-            static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, r.worker_high_water.size()) * 8));
-        for (size_t i = 0; i < r.worker_nodes.size(); ++i) {
-            out->worker_nodes[i] = r.worker_nodes[i];
-            out->worker_stack_high_water[i] = r.worker_high_water[i];
+        // WorkerMetrics per reference worker: a hybrid solve that filled the device reports its
+        // device workers folded into the configured num_workers (device worker i counts for
+        // worker i % num_workers; stack high water = the maximum)
+        const size_t dw = r.worker_nodes.size();
+        const bool fold = p->strategy == VCG_HYBRID && !p->device_workers && p->workers && dw;
+        const size_t nw = fold ? p->workers : dw;
+        out->num_workers = (uint32_t)nw;
+        out->worker_nodes = static_cast<uint64_t*>(std::calloc(std::max<size_t>(1, nw), 8));
+        out->worker_stack_high_water = static_cast<uint64_t*>(std::calloc(std::max<size_t>(1, nw), 8));
+        for (size_t i = 0; i < dw; ++i) {
+            const size_t j = fold ? i % nw : i;
+            out->worker_nodes[j] += r.worker_nodes[i];
+            out->worker_stack_high_water[j] =
+                std::max<uint64_t>(out->worker_stack_high_water[j], r.worker_high_water[i]);
             out->nodes_total += r.worker_nodes[i];
         }
         out->wl_added = r.wl_added;

@@ -484,6 +484,7 @@ struct DenseRun {
         a.seq_mode = s.strategy != 0 ? 1 : 0;  // seq and stackonly never donate
         a.donate_oldest = s.donate_oldest ? 1 : 0;
         a.compact = s.engine == 3 ? 0 : 1;
+        a.mid = (s.engine == 3 || s.engine == 4) ? 0 : 1;
         a.stackonly = s.strategy == 2 ? 1 : 0;
         a.depth = s.depth;
         a.mailbox = s.mailbox;
@@ -797,7 +798,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     uint64_t ring = 2;
     while (ring < cap) ring <<= 1;
     // per worker: 10n u32 lists, n u32 counters, n u64 claims, n u32 tags
-    const size_t scratch_bytes = (size_t)workers * g.n * (10 * 4 + 4 + 8 + 4);
+    const size_t scratch_bytes = (size_t)workers * g.n * (12 * 4 + 4 + 8 + 4);
     const size_t fixed = ring * entry + ring * 8 + scratch_bytes + (64ull << 20);
     if (fixed >= free_b) throw std::runtime_error("CUDA error: out of device memory for the worklist");
     const uint64_t by_mem = (uint64_t)((free_b - fixed) * 0.6 / ((double)workers * entry));
@@ -816,8 +817,8 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     const size_t wn = (size_t)workers * g.n;
     unsigned long long* owner = reinterpret_cast<unsigned long long*>(scr);  // 8-aligned first
     uint32_t* scratch = reinterpret_cast<uint32_t*>(scr + wn * 8);
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(scr + wn * 48);
-    uint32_t* tag = reinterpret_cast<uint32_t*>(scr + wn * 52);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(scr + wn * 56);
+    uint32_t* tag = reinterpret_cast<uint32_t*>(scr + wn * 60);
     CUDA_CHECK(cudaMemsetAsync(cnt, 0, wn * 4, st));        // counters start at zero
     CUDA_CHECK(cudaMemsetAsync(owner, 0xFF, wn * 8, st));   // no triangle claims
     CUDA_CHECK(cudaMemsetAsync(tag, 0, wn * 4, st));        // epochs start at 1

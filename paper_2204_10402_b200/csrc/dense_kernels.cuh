@@ -129,6 +129,8 @@ struct DenseArgs {
     int seq_mode;             // never donate (solve_*_seq semantics)
     int donate_oldest;        // donate the bottom (oldest) stacked node instead of the new child
     int compact;              // renumber nodes with <= 64 alive vertices (CompactNode)
+    int mid;                  // (W >= 16) renumber nodes with <= 128 alive vertices into a
+                              // per-warp frame (the mid layout, WarpNode<4, ., W>)
     int stackonly;            // StackOnly strategy (scheduler.cpp:214-297): claim sub-tree ids
     uint32_t depth;           // StackOnly sub-tree depth (2^depth sub-trees)
     volatile uint32_t* mailbox;  // host-mapped: [0] ext best in, [1] cancel in, [2] best out,
@@ -273,7 +275,7 @@ __device__ __forceinline__ void reset_deltas(Counters32& st) {
 // Cover count of a stacked marker standing for a child proven pruned at birth.
 constexpr uint32_t DEAD_NODE = 0xFFFFFFFFu;
 // Record kinds (header word 2): wide (WarpNode layout) or compact (CompactNode layout).
-constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1;
+constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1, REC_MID = 2;
 
 #ifndef VCG_POLL_EVERY
 #define VCG_POLL_EVERY 32  // nodes between reads of the control line (power of two; C5: 4 → 12.3 ms,
@@ -307,23 +309,32 @@ __device__ __forceinline__ uint32_t dense_degree_base(uint32_t wib) {
     return dense_scratch_base<W>(8) + wib * W * 32;
 }
 
-template <int W, bool INSTR>
+// WG == 0: the WIDE layout over the whole graph (vertex v at lane v & 31, word v >> 5). WG != 0:
+// the MID layout (induced, "frame" renumbering): at most 32*W alive vertices of a graph of width WG
+// renumbered in id order into slots, their induced adjacency rows in a per-warp FRAME bitmap in
+// shared memory, degrees in registers. Every primitive is the wide one on a W-word bitmap, so
+// the same reduce_node runs on it and, slots keeping the id order, acts on the same vertices.
+template <int W, bool INSTR, int WG = 0>
 struct WarpNode {
     static constexpr bool kInstr = INSTR;
+    static constexpr bool IND = WG != 0;
+    static constexpr int kW = W;
     static constexpr int kPassUnroll = 1;  // (rolled: the wide pass body is large)
     static constexpr int Q = W / 4;  // uint4 groups per bitmap row
+    // Wide degrees live in the warp's shared slots (VCG_WIDE_SMEM): the wide layout then holds
+    // no degree registers, so the kernel's register budget (and with it the occupancy of the
+    // compact hot path) is set by the compact layout. The mid layout keeps its W in registers.
 #if VCG_WIDE_SMEM
-    // degree of vertex 32*i + lane (meaningless once removed), in the warp's shared slots: the
-    // wide layout then holds no degree registers, so the kernel's register budget (and with
-    // it the occupancy of the compact hot path) is set by the compact layout
-    uint32_t dsb;                    // u32 index of this warp's W x 32 degree words
-    __device__ __forceinline__ uint32_t& D(int i) const {
-        return reinterpret_cast<uint32_t*>(dense_smem)[dsb + i * 32 + lane];
-    }
+    static constexpr bool kDegSmem = !IND;
 #else
-    mutable uint32_t d[W];           // degree of vertex 32*i + lane (meaningless once removed)
-    __device__ __forceinline__ uint32_t& D(int i) const { return d[i]; }
+    static constexpr bool kDegSmem = false;
 #endif
+    uint32_t dsb;                    // u32 index of this warp's W x 32 degree words (kDegSmem)
+    mutable uint32_t dr[kDegSmem ? 1 : W];  // degree of vertex 32*i + lane (!kDegSmem)
+    __device__ __forceinline__ uint32_t& D(int i) const {
+        if constexpr (kDegSmem) return reinterpret_cast<uint32_t*>(dense_smem)[dsb + i * 32 + lane];
+        else return dr[i];
+    }
     uint32_t alv;                    // bit i: vertex 32*i + lane is alive (not in the cover)
     uint32_t aw;                     // lane j < W: alive bitmap word j (vertices 32j..32j+31)
     uint32_t nt;                     // bit i: vertex 32*i + lane has degree two and was found
@@ -335,17 +346,23 @@ struct WarpNode {
     static constexpr uint32_t NPAD = 32 * W;  // bitmap columns (vertex slots)
     uint32_t ssb;                    // u32 index of this warp's W x 32 scratch words
     int lane;
+    // mid layout only: the frame
+    uint32_t rb;                     // uint4 index of the frame bitmap ([Q][NPAD] uint4 groups)
+    uint32_t idb;                    // u16 index of the frame's slot -> vertex id table (32W)
+    uint32_t tgi;                    // u64 index of this warp's current frame tag
+    uint32_t ns;                     // uniform: slots of the frame
 
-    __device__ __forceinline__ static const uint4& grp(uint32_t q, uint32_t v) {
-        return dense_smem[q * NPAD + v];  // row v, words 4q..4q+3
+    __device__ __forceinline__ const uint4& grp(uint32_t q, uint32_t v) const {
+        if constexpr (IND) return dense_smem[rb + q * NPAD + v];
+        else return dense_smem[q * NPAD + v];  // row v, words 4q..4q+3
     }
     __device__ __forceinline__ uint32_t& scratch(int i) const {
         return reinterpret_cast<uint32_t*>(dense_smem)[ssb + i * 32 + lane];
     }
-
     __device__ __forceinline__ bool alive(int i) const { return (alv >> i) & 1u; }
     __device__ __forceinline__ uint32_t row_word(uint32_t u, uint32_t j) const {
-        return reinterpret_cast<const uint32_t*>(dense_smem)[((j >> 2) * NPAD + u) * 4 + (j & 3)];
+        const uint32_t b = IND ? rb * 4 : 0u;
+        return reinterpret_cast<const uint32_t*>(dense_smem)[b + ((j >> 2) * NPAD + u) * 4 + (j & 3)];
     }
     __device__ __forceinline__ void rebuild_aw() {
 #pragma unroll
@@ -478,8 +495,9 @@ struct WarpNode {
         store_child(c.keepm, c.xcnt, rec);
     }
     template <int WW>
-    __device__ __forceinline__ uint32_t cover_word(uint32_t*) const {
-        return cover_word();
+    __device__ __forceinline__ uint32_t cover_word(uint32_t* sb) const {
+        if constexpr (IND) return mid_cover_word(sb);
+        else return cover_word();
     }
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
@@ -541,6 +559,13 @@ struct WarpNode {
     }
     __device__ __forceinline__ void store_child(uint32_t keepm, uint32_t xcnt,
                                                 unsigned char* rec) const {
+        if constexpr (IND) {
+            uint32_t esum = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) esum += ((keepm >> i) & 1u) ? D(i) - scratch(i) : 0u;
+            store_mid(rec, cc + xcnt, __reduce_add_sync(FULL, esum) / 2, keepm, nt & keepm);
+            return;
+        }
         uint32_t packed[W / 2];
         uint32_t esum = 0;
 #pragma unroll
@@ -573,6 +598,10 @@ struct WarpNode {
         }
     }
     __device__ __forceinline__ void store_current(unsigned char* rec) const {
+        if constexpr (IND) {
+            store_mid(rec, cc, edges, alv, nt);
+            return;
+        }
         uint32_t packed[W / 2];
 #pragma unroll
         for (int i = 0; i < W; ++i) {
@@ -586,6 +615,10 @@ struct WarpNode {
     }
     // Loads a record through L2 (it may come from another SM's worklist donation).
     __device__ __forceinline__ void load(const unsigned char* rec) {
+        if constexpr (IND) {
+            load_mid(rec);
+            return;
+        }
         uint32_t packed[W / 2];
         const unsigned char* p = rec + 16 + lane * (2 * W);
         if constexpr (W == 4) {
@@ -627,6 +660,197 @@ struct WarpNode {
             if (lane == i) mine = b;
         }
         return mine;
+    }
+
+    // ---- the mid layout's frame and records (IND)
+    //
+    // Record: {cc, edges, REC_MID, ns} {tag lo, tag hi, 0, 0} + alive words (W u32, word j =
+    // slots 32j..32j+31) + per-lane cached verdicts (32 u32) + the frame's slot -> vertex ids
+    // (32W u16). Degrees are not stored: they are the popcounts of the alive rows. A record is
+    // reloaded on the frame it was made on when the warp still holds that frame (the tag
+    // matches: its own depth-first subtree); otherwise (a donated record, or the warp has moved
+    // on) its alive vertices are renumbered into a fresh frame (rebuild).
+    static constexpr uint32_t kMidNt = 32 + 4 * W, kMidIds = 32 + 4 * W + 128;
+    static constexpr uint32_t kMidBytes = kMidIds + 64 * W;
+    __device__ __forceinline__ uint32_t graph_id(uint32_t slot) const {
+        return reinterpret_cast<const uint16_t*>(dense_smem)[idb + slot];
+    }
+    __device__ __forceinline__ unsigned long long& frame_tag() const {
+        return reinterpret_cast<unsigned long long*>(dense_smem)[tgi];
+    }
+    __device__ __forceinline__ void store_mid(unsigned char* rec, uint32_t rcc, uint32_t redges,
+                                              uint32_t keep, uint32_t rnt) const {
+        uint32_t word = 0;  // alive word `lane` (< W)
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const uint32_t b = __ballot_sync(FULL, (keep >> i) & 1u);
+            if (lane == i) word = b;
+        }
+        if (lane == 0) {
+            const unsigned long long t = frame_tag();
+            reinterpret_cast<uint4*>(rec)[0] = make_uint4(rcc, redges, REC_MID, ns);
+            reinterpret_cast<uint4*>(rec)[1] = make_uint4((uint32_t)t, (uint32_t)(t >> 32), 0u, 0u);
+        }
+        if (lane < W) reinterpret_cast<uint32_t*>(rec + 32)[lane] = word;
+        reinterpret_cast<uint32_t*>(rec + kMidNt)[lane] = rnt;
+        // ids: 32W u16 = 2W bytes per lane
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(dense_smem) + 2 * idb;
+        if constexpr (W == 4)
+            reinterpret_cast<uint2*>(rec + kMidIds)[lane] = reinterpret_cast<const uint2*>(src)[lane];
+        else
+#pragma unroll
+            for (int t = 0; t < W / 8; ++t)
+                reinterpret_cast<uint4*>(rec + kMidIds)[lane + 32 * t] =
+                    reinterpret_cast<const uint4*>(src)[lane + 32 * t];
+    }
+    // degrees = popcounts of the alive induced rows (aw words gathered on every lane)
+    __device__ __forceinline__ void set_degrees() {
+        uint32_t a[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) a[j] = __shfl_sync(FULL, aw, j);
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            uint32_t d = 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const uint4 r = grp(q, 32 * i + lane);
+                d += __popc(r.x & a[4 * q]) + __popc(r.y & a[4 * q + 1]) +
+                     __popc(r.z & a[4 * q + 2]) + __popc(r.w & a[4 * q + 3]);
+            }
+            D(i) = alive(i) ? d : 0u;
+        }
+    }
+    // A fresh frame over the nalive vertices whose ids are in the frame id table (ascending):
+    // induced rows by ballots — lane l tests A[id(32i + l)][id(t)], so by symmetry the W
+    // ballots for slot t are row t — then alive masks, degrees and a new tag.
+    // (the warp's tag counter sits right after its current tag: tags are unique per shard, warp
+    // and frame — (rank << 56) | ((worker + 1) << 36) | count, set up by the kernel)
+    __device__ __forceinline__ unsigned long long next_tag() const {
+        unsigned long long t = 0;
+        if (lane == 0) t = ++reinterpret_cast<unsigned long long*>(dense_smem)[tgi + 1];
+        return __shfl_sync(FULL, t, 0);
+    }
+    template <int GW>
+    __device__ __noinline__ void build_frame(uint32_t nalive) {
+        const unsigned long long tag = next_tag();
+        constexpr uint32_t GNPAD = 32 * GW;
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(dense_smem);
+        uint32_t myid[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) myid[i] = 32 * i + lane < nalive ? graph_id(32 * i + lane) : 0xFFFFu;
+#pragma unroll 1
+        for (uint32_t t = 0; t < nalive; ++t) {
+            const uint32_t idt = graph_id(t);
+            const uint32_t wj = idt >> 5, bit = idt & 31u;
+            uint32_t row[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const bool b = myid[i] != 0xFFFFu &&
+                               ((gw[((wj >> 2) * GNPAD + myid[i]) * 4 + (wj & 3)] >> bit) & 1u);
+                row[i] = __ballot_sync(FULL, b);
+            }
+            if (lane < Q)
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    if (lane == q)
+                        dense_smem[rb + q * NPAD + t] =
+                            make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+        }
+        alv = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) alv |= (32u * i + lane < nalive ? 1u : 0u) << i;
+        ns = nalive;
+        nt = 0;  // (verdicts are a cache: starting empty only re-runs tests)
+        __syncwarp();
+        rebuild_aw();
+        set_degrees();
+        if (lane == 0) frame_tag() = tag;
+        __syncwarp();
+    }
+    // Renumbers a reduced wide node with at most 32W alive vertices into a fresh frame.
+    template <bool I2>
+    __device__ __forceinline__ void from_wide(const WarpNode<WG, I2>& w) {
+        cc = w.cc;
+        edges = w.edges;
+        doom = false;
+        const uint32_t pc = lane < WG ? __popc(w.aw) : 0u;
+        uint32_t incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t base = incl - pc;  // lane j < WG: first slot of word j
+        const uint32_t nalive = __shfl_sync(FULL, incl, 31);
+        uint16_t* sid = reinterpret_cast<uint16_t*>(dense_smem) + idb;
+#pragma unroll 1
+        for (int i = 0; i < WG; ++i) {
+            const uint32_t awi = __shfl_sync(FULL, w.aw, i);
+            const uint32_t bi = __shfl_sync(FULL, base, i);
+            if ((w.alv >> i) & 1u) sid[bi + __popc(awi & ((1u << lane) - 1u))] = (uint16_t)(32 * i + lane);
+        }
+        __syncwarp();
+        build_frame<WG>(nalive);
+    }
+    // Loads a mid record: on the frame it was made on if the warp holds it, else renumbered
+    // into a fresh frame.
+    __device__ __forceinline__ void load_mid(const unsigned char* rec) {
+        uint4 h0 = make_uint4(0, 0, 0, 0);
+        uint2 h1 = make_uint2(0, 0);
+        int same = 0;
+        if (lane == 0) {
+            h0 = __ldcg(reinterpret_cast<const uint4*>(rec));
+            h1 = __ldcg(reinterpret_cast<const uint2*>(rec + 16));
+            same = frame_tag() == (((unsigned long long)h1.y << 32) | h1.x);
+        }
+        cc = __shfl_sync(FULL, h0.x, 0);
+        edges = __shfl_sync(FULL, h0.y, 0);
+        doom = false;
+        aw = lane < W ? __ldcg(reinterpret_cast<const uint32_t*>(rec + 32) + lane) : 0u;
+        if (__shfl_sync(FULL, same, 0)) {
+            ns = __shfl_sync(FULL, h0.w, 0);
+            alv = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) alv |= ((__shfl_sync(FULL, aw, i) >> lane) & 1u) << i;
+            nt = __ldcg(reinterpret_cast<const uint32_t*>(rec + kMidNt) + lane);
+            set_degrees();
+            return;
+        }
+        rebuild_from(rec);
+    }
+    // The record's alive vertices (ids through its own id table) renumbered into a fresh frame.
+    __device__ __noinline__ void rebuild_from(const unsigned char* rec) {
+        uint32_t a[W], below[W];
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            a[j] = __shfl_sync(FULL, aw, j);
+            below[j] = run;
+            run += __popc(a[j]);
+        }
+        const uint16_t* rid = reinterpret_cast<const uint16_t*>(rec + kMidIds);
+        uint16_t* sid = reinterpret_cast<uint16_t*>(dense_smem) + idb;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if ((a[j] >> lane) & 1u)
+                sid[below[j] + __popc(a[j] & ((1u << lane) - 1u))] = __ldcg(rid + 32 * j + lane);
+        __syncwarp();
+        build_frame<WG>(run);
+    }
+    // Word `lane` (< WG) of the cover bitmap (graph vertices not alive), in shared scratch.
+    __device__ __forceinline__ uint32_t mid_cover_word(uint32_t* sb) const {
+        if (lane < WG) sb[lane] = FULL;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (alive(i)) {
+                const uint32_t id = graph_id(32 * i + lane);
+                atomicAnd(&sb[id >> 5], ~(1u << (id & 31)));
+            }
+        __syncwarp();
+        const uint32_t w = lane < WG ? sb[lane] : 0u;
+        __syncwarp();
+        return w;
     }
 };
 
@@ -791,8 +1015,8 @@ struct CompactNode {
     }
     // Renumbers a reduced wide node with at most 64 alive vertices. `sb` is the warp's shared
     // scratch (at least 64 u16 + W words).
-    template <int W, bool I2>
-    __device__ __forceinline__ void from_wide(const WarpNode<W, I2>& w, uint32_t* sb) {
+    template <int W, bool I2, int WG2>
+    __device__ __forceinline__ void from_wide(const WarpNode<W, I2, WG2>& w, uint32_t* sb) {
         lane = w.lane;
         cc = w.cc;
         edges = w.edges;
@@ -821,7 +1045,11 @@ struct CompactNode {
         __syncwarp();
         const uint32_t id0 = sid[lane], id1 = sid[lane + 32];
         __syncwarp();
-        ids = id0 | (id1 << 16);
+        if constexpr (WG2 != 0)  // from a mid node: slots -> graph ids through its frame
+            ids = (id0 != 0xFFFFu ? w.graph_id(id0) : 0xFFFFu) |
+                  ((id1 != 0xFFFFu ? w.graph_id(id1) : 0xFFFFu) << 16);
+        else
+            ids = id0 | (id1 << 16);
         am = nalive >= 64 ? ~0ull : ((1ull << nalive) - 1ull);
         nt = 0;  // (verdicts are a cache: starting empty only re-runs tests)
 #if VCG_FROM_WIDE_BALLOT
@@ -967,9 +1195,9 @@ __device__ __forceinline__ void reduce_node(N& x, int B, Cnt& st) {
     }
 }
 
-template <int W, bool INSTR>
+template <int W, bool INSTR, int WG>
 template <class Cnt>
-__device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int B, Cnt& st) {
+__device__ __forceinline__ void WarpNode<W, INSTR, WG>::reduce(int B, Cnt& st) {
     reduce_node(*this, B, st);
 }
 // The wide reduction out of line (VCG_WIDE_NOINLINE): the wide layout is the cold one, and its
@@ -978,8 +1206,8 @@ __device__ __forceinline__ void WarpNode<W, INSTR>::reduce(int B, Cnt& st) {
 struct RuleDeltas {
     uint32_t rounds, rm1, rm2, rmh;
 };
-template <int W>
-__device__ __noinline__ RuleDeltas wide_reduce(WarpNode<W, false>& x, int B) {
+template <class N>
+__device__ __noinline__ RuleDeltas wide_reduce(N& x, int B) {
     CountersT<uint32_t> c;
     reduce_node(x, B, c);
     return RuleDeltas{c.rounds, c.rm1, c.rm2, c.rmh};
@@ -1146,9 +1374,15 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // (the warp's W-word slot between the bitmap and the scratch words; W >= 4)
     unsigned long long* const t0s = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
+    // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
+    constexpr int MW = W >= 16 ? 4 : 0;  // mid layout width (words per frame row)
     if (lane == 0) {
         t0s[0] = globaltimer();
         t0s[1] = (unsigned long long)clock64();
+        if (MW) {
+            t0s[2] = 0;  // no frame
+            t0s[3] = ((unsigned long long)a.rank << 56) | ((unsigned long long)(worker + 1) << 36);
+        }
     }
     __syncwarp();
 #define t_start (t0s[0])
@@ -1163,7 +1397,16 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     x.lane = lane;
     CompactNode<INSTR> y;
     y.lane = lane;
-    bool compact = false;
+    // the mid layout (64 < alive <= 32 MW): its frame bitmap in the warp's wide degree words,
+    // its scratch and frame id table in the warp's wide scratch words (unused while mid)
+    WarpNode<MW ? MW : 4, INSTR, W> m;
+    m.lane = lane;
+    m.ssb = x.ssb;
+    m.rb = dense_degree_base<W>(wib) / 4;
+    m.idb = (x.ssb + (MW ? MW : 4) * 32) * 2;
+    m.tgi = (uint32_t)(reinterpret_cast<uint32_t*>(t0s) - reinterpret_cast<uint32_t*>(dense_smem)) / 2 + 2;
+    enum { M_WIDE = 0, M_COMPACT = 1, M_MID = 2 };
+    uint32_t mode = M_WIDE;
     // (derived on use rather than held in registers: the hot path's register budget sets the
     // occupancy)
 #define sb (reinterpret_cast<uint32_t*>(dense_smem) + x.ssb)  // warp scratch
@@ -1203,10 +1446,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto reduce_under_B = [&](auto& n) {
-        if constexpr (VCG_WIDE_NOINLINE && !INSTR &&
-                      std::is_same<typename std::remove_reference<decltype(n)>::type,
-                                   WarpNode<W, INSTR>>::value) {
-            const RuleDeltas dl = wide_reduce<W>(n, B);
+        using NT = typename std::remove_reference<decltype(n)>::type;
+        if constexpr (VCG_WIDE_NOINLINE && !INSTR && !std::is_same<NT, CompactNode<INSTR>>::value) {
+            const RuleDeltas dl = wide_reduce(n, B);
             st.rounds += dl.rounds;
             st.rm1 += dl.rm1;
             st.rm2 += dl.rm2;
@@ -1423,11 +1665,27 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 src = a.wl + (pos & a.ring_mask) * a.entry_bytes;
                 idle = false;
             }
-            uint32_t kind = 0;
-            if (lane == 0) kind = __ldcg(reinterpret_cast<const uint32_t*>(src) + 2);
-            compact = __shfl_sync(FULL, kind, 0) == REC_COMPACT;
-            if (compact) y.load(src);
-            else x.load(src);
+            uint2 kc = make_uint2(0, 0);  // {cover count, kind}
+            if (lane == 0) {
+                const uint4 hd = __ldcg(reinterpret_cast<const uint4*>(src));
+                kc = make_uint2(hd.x, hd.z);
+            }
+            const uint32_t kind = __shfl_sync(FULL, kc.y, 0);
+            if (kind == REC_COMPACT) {
+                mode = M_COMPACT;
+                y.load(src);
+            } else if (MW && kind == REC_MID) {
+                mode = M_MID;
+                m.load(src);
+            } else {
+                mode = M_WIDE;
+                if (seq_mode_ && __shfl_sync(FULL, kc.x, 0) == DEAD_NODE) {
+                    x.cc = DEAD_NODE;  // a dead child's marker (see below): nothing to load
+                } else {
+                    x.load(src);
+                    if (MW && lane == 0) t0s[2] = 0;  // the wide degrees overwrote the frame
+                }
+            }
             if (release) {
                 // every lane's read of the slot is ordered before lane 0's release by the
                 // warp barrier (cumulativity): no full fence needed
@@ -1496,22 +1754,35 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
 
         // a doomed child's marker: visited, pruned (markers exist only in the one-worker
         // strategies; the hybrid kernel never reads the wide node's local-memory copy here)
-        if (seq_mode_ && (compact ? y.cc : x.cc) == DEAD_NODE) {
+        if (seq_mode_ && mode == M_WIDE && x.cc == DEAD_NODE) {
             ++st.dooms;
             have = false;
             continue;
         }
         int act;
-        if (compact) {
+        if (mode == M_COMPACT) {
             act = settle(y);
+        } else if (MW && mode == M_MID) {
+            act = settle(m);
+            if (act == ACT_BRANCH && m.alive_count() <= kCompactSlots) {
+                y.from_wide(m, sb);
+                mode = M_COMPACT;
+            }
         } else {
             act = settle(x);
-            if (act == ACT_BRANCH && a.compact && x.alive_count() <= kCompactSlots) {
-                y.from_wide(x, sb);
-                compact = true;
+            if (act == ACT_BRANCH && a.compact) {
+                const uint32_t na = x.alive_count();
+                if (na <= kCompactSlots) {
+                    y.from_wide(x, sb);
+                    mode = M_COMPACT;
+                } else if (MW && a.mid && na <= 32u * MW) {
+                    m.from_wide(x);
+                    mode = M_MID;
+                }
             }
         }
-        if (act == ACT_BRANCH) act = compact ? branch(y) : branch(x);
+        if (act == ACT_BRANCH)
+            act = mode == M_COMPACT ? branch(y) : (MW && mode == M_MID) ? branch(m) : branch(x);
         if (act == ACT_BREAK) break;
         if (act == ACT_POP) have = false;
     }

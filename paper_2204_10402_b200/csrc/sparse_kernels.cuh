@@ -48,7 +48,7 @@ struct SparseArgs {
     uint32_t* cover_slots;    // workers * cover_words
     uint32_t cover_words;     // ceil(n / 32)
     WStats* stats;
-    uint32_t* scratch;        // workers * 8n u32: A1, A2, N1, N2, L3, RL, T, P(2n) ...
+    uint32_t* scratch;        // workers * 12n u32: A1, A2, N1, N2, L3, RL, T, P(2n), L, PP(2n)
     unsigned long long* owner;  // workers * n (triangle claims, epoch-tagged)
     uint32_t* tag;            // workers * n (phase / branch-set membership, epoch-tagged)
     uint32_t* cnt;            // workers * n (per-vertex counters, zero between uses)
@@ -154,6 +154,8 @@ struct CtaNode {
     const SparseArgs* a;
     uint32_t *A1, *A2, *N1, *N2;  // candidate lists: this round (A) and the next (N)
     uint32_t *L3, *RL, *T, *P;    // above-limit list, removal list, triangle proposers/partners
+    uint32_t *L, *PP;             // candidates still at degree one / two; their alive partners
+                                  // (PP[2v], PP[2v+1], indexed by vertex)
     uint32_t* cnt;
     unsigned long long* owner;
     uint32_t* tag;
@@ -314,12 +316,46 @@ struct CtaNode {
         append(got, u, RL, &sh->nrem);
     }
 
+    // The alive partners of the candidates in `list` that still have degree `d` (1 or 2): the
+    // candidates go to L (count in s.nA), their partners to PP[2v..]. The adjacency slices are
+    // walked load-balanced over the whole block (for_each_neighbor): a per-thread walk of one
+    // slice is a chain of dependent L2 loads as long as the vertex's ORIGINAL degree — a hub
+    // that dropped to degree one kept every other thread waiting at the next barrier.
+    __device__ void find_partners(const uint32_t* list, uint32_t count, uint32_t d) {
+        SpShared& s = *sh;
+        if (threadIdx.x == 0) s.nA = 0;
+        __syncthreads();
+        for (uint32_t base = 0; base < count; base += SP_THREADS) {
+            const uint32_t i = base + threadIdx.x;
+            const uint32_t v = i < count ? list[i] : 0u;
+            append(i < count && deg[v] == d, v, L, &s.nA);
+        }
+        __syncthreads();
+        const uint16_t* dg = deg;
+        uint32_t* ct = cnt;
+        uint32_t* pp = PP;
+        for_each_neighbor(L, s.nA, [&](bool valid, uint32_t v, uint32_t w) {
+            if (valid && dg[w] != DREM) {
+                if (d == 1) {
+                    pp[2 * v] = w;  // the unique alive neighbour
+                } else {
+                    // (bounded: a candidate listed twice walks its slice twice; the first two
+                    // partners found are then not necessarily distinct, which only skips a
+                    // reduction — never unsound)
+                    const uint32_t slot = atomicAdd(ct + v, 1u);
+                    if (slot < 2) pp[2 * v + slot] = w;
+                }
+            }
+        });
+    }
+
     // degree one over A1 (entries whose degree is still 1); new degree-1 vertices go to N1
     // (next round), new degree-2 ones to A2 (this round's degree-two phase)
     __device__ uint32_t phase_degree_one() {
         SpShared& s = *sh;
-        const uint32_t c = s.a1;
         const uint32_t ep = ++epoch;
+        find_partners(A1, s.a1, 1);
+        const uint32_t c = s.nA;
         if (threadIdx.x == 0) s.nrem = 0;
         __syncthreads();
         for (uint32_t base = 0; base < c; base += SP_THREADS) {
@@ -327,19 +363,10 @@ struct CtaNode {
             bool take = false;
             uint32_t u = 0;
             if (i < c) {
-                const uint32_t v = A1[i];
-                if (deg[v] == 1) {
-                    for (uint32_t e = a->off[v]; e < a->off[v + 1]; ++e) {
-                        const uint32_t w = a->nbr[e];
-                        if (deg[w] != DREM) {
-                            u = w;
-                            take = true;
-                            break;
-                        }
-                    }
-                    // isolated edge: the smaller id acts (reductions.cpp:7-19 visits it first)
-                    if (take && deg[u] == 1 && u < v) take = false;
-                }
+                const uint32_t v = L[i];
+                u = PP[2 * v];
+                // isolated edge: the smaller id acts (reductions.cpp:7-19 visits it first)
+                take = !(deg[u] == 1 && u < v);
             }
             claim_into_rl(take, u, ep);
         }
@@ -352,9 +379,10 @@ struct CtaNode {
     // degree two over A2 (entries whose degree is still 2); new candidates go to N1 / N2
     __device__ uint32_t phase_degree_two() {
         SpShared& s = *sh;
-        const uint32_t c = s.a2;
         const uint32_t ep = ++epoch;
         const unsigned long long key_hi = (unsigned long long)(~ep) << 32;
+        find_partners(A2, s.a2, 2);
+        const uint32_t c = s.nA;
         if (threadIdx.x == 0) {
             s.nT = 0;
             s.nrem = 0;
@@ -365,18 +393,12 @@ struct CtaNode {
             bool tri = false;
             uint32_t v = 0, p0 = 0, p1 = 0;
             if (i < c) {
-                v = A2[i];
-                if (deg[v] == 2) {
-                    int f = 0;
-                    for (uint32_t e = a->off[v]; e < a->off[v + 1] && f < 2; ++e) {
-                        const uint32_t w = a->nbr[e];
-                        if (deg[w] != DREM) {
-                            if (f == 0) p0 = w;
-                            else p1 = w;
-                            ++f;
-                        }
-                    }
-                    tri = f == 2 && has_edge(p0, p1);
+                v = L[i];
+                {
+                    p0 = PP[2 * v];
+                    p1 = PP[2 * v + 1];
+                    cnt[v] = 0;  // (counters are zero between uses)
+                    tri = has_edge(p0, p1);
                     if (tri) {
                         const unsigned long long key = key_hi | v;
                         atomicMin(owner + v, key);
@@ -629,7 +651,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
     x.cstart = x.cbuf + SP_THREADS;
     x.sh = &sh;
     x.a = &a;
-    uint32_t* scr = a.scratch + (unsigned long long)worker * 10ull * a.n;
+    uint32_t* scr = a.scratch + (unsigned long long)worker * 12ull * a.n;
     x.A1 = scr;
     x.A2 = scr + 1ull * a.n;
     x.N1 = scr + 2ull * a.n;
@@ -638,6 +660,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
     x.RL = scr + 5ull * a.n;
     x.T = scr + 6ull * a.n;
     x.P = scr + 7ull * a.n;  // 2n
+    x.L = scr + 9ull * a.n;
+    x.PP = scr + 10ull * a.n;  // 2n
     x.cnt = a.cnt + (unsigned long long)worker * a.n;
     x.owner = a.owner + (unsigned long long)worker * a.n;
     x.tag = a.tag + (unsigned long long)worker * a.n;

@@ -63,9 +63,10 @@ def test_corpus_hybrid_oracle_equivalence(corpus, workers, capacity, fraction):
     bad = []
     for it in corpus[::3]:
         g = graph_of(it)
-        strategy = "gpu" if workers is None else "hybrid"
-        r = vc.solve_mvc(g, strategy=strategy, workers=workers, capacity=capacity,
-                         threshold_fraction=fraction)
+        # fixed small device worker counts run the reference's donation policy
+        kw = dict(strategy="gpu") if workers is None else dict(strategy="hybrid",
+                                                                device_workers=workers)
+        r = vc.solve_mvc(g, capacity=capacity, threshold_fraction=fraction, **kw)
         check_cover(g, r)
         w = r["worklist"]
         if (r["size"] != it["mvc"] or r["status"] != "complete" or w["added"] != w["removed"]
@@ -82,7 +83,7 @@ def test_corpus_pvc_triple_hybrid(corpus, workers):
         g = graph_of(it)
         for p in it["pvc"]:
             r = vc.solve_pvc(g, p["k"], strategy="gpu" if workers is None else "hybrid",
-                             workers=workers, capacity=64)
+                             device_workers=workers, capacity=64)
             ok = r["feasible"] == p["feasible"]
             if r["feasible"]:
                 check_cover(g, r)
@@ -136,7 +137,7 @@ def test_budget_and_timeout_status():
     r = vc.solve_mvc(g, strategy="gpu", node_budget=1000)
     assert r["status"] == "budget"
     check_cover(g, r)  # best-so-far certificate stays valid (test_scheduler.cpp:175-189)
-    r = vc.solve_mvc(g, strategy="hybrid", workers=1, timeout_s=0.0)
+    r = vc.solve_mvc(g, strategy="hybrid", device_workers=1, timeout_s=0.0)
     assert r["status"] == "timeout"
     check_cover(g, r)
 
@@ -154,6 +155,22 @@ def test_report_shape():
     ratios = rep["load_ratios"]
     assert abs(sum(ratios) / len(ratios) - 1.0) < 1e-9
     assert sum(rep["phase_shares"].values()) <= 1.0 + 1e-9
+
+
+def test_hybrid_reference_defaults_fill_the_device(config_golden):
+    """solve_mvc(g) with the reference's defaults (hybrid, 4 workers) runs every resident warp
+    of the device and folds them into the 4 report entries the reference's callers expect."""
+    g = load_config("c1")
+    r = vc.solve_mvc(g)
+    assert r["size"] == config_golden["c1"]["mvc"] and r["workers"] == 4
+    assert len(r["worker_nodes"]) == 4 and sum(r["worker_nodes"]) == r["nodes_total"]
+    assert r["grid_blocks"] * r["block_threads"] // 32 >= 1000
+    no = vc.solve_pvc(g, config_golden["c1"]["pvc_no_k"])
+    assert not no["feasible"] and no["nodes_total"] == config_golden["c1"]["pvc_no_nodes"]
+    assert len(no["worker_nodes"]) == 4
+    few = vc.solve_mvc(g, device_workers=8)
+    assert few["grid_blocks"] * few["block_threads"] // 32 >= 8
+    assert len(few["worker_nodes"]) == 8
 
 
 def test_instrumented_phase_shares():
@@ -222,8 +239,8 @@ def test_sparse_engine_corpus_exact(corpus, workers):
     bad = []
     for it in corpus:
         g = graph_of(it)
-        r = vc.solve_mvc(g, strategy="gpu" if workers is None else "hybrid", workers=workers,
-                         engine="sparse")
+        r = vc.solve_mvc(g, strategy="gpu" if workers is None else "hybrid",
+                         device_workers=workers, engine="sparse")
         check_cover(g, r)
         if r["size"] != it["mvc"] or r["status"] != "complete" or r["engine"] != 2:
             bad.append((it["name"], r["size"], it["mvc"]))
@@ -484,7 +501,7 @@ def test_parallel_mvc_is_exact_without_certificate(oracle, name):
     off, nbr = g.csr()
     want = oracle.solve_seq(CSR(g.num_vertices, g.num_edges, off, nbr))
     for kw in (dict(strategy="gpu"), dict(strategy="hybrid", workers=3552),
-               dict(strategy="hybrid", workers=64),
+               dict(strategy="hybrid", workers=64), dict(strategy="hybrid", device_workers=64),
                dict(strategy="gpu", engine="dense-wide"), dict(strategy="gpu", engine="sparse"),
                dict(strategy="stackonly", workers=1024, depth=12)):
         for _ in range(8):
