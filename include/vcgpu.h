@@ -5,6 +5,17 @@
  * (VCG_OK = 0); on failure vcg_last_error() holds a thread-local message whose text follows the
  * reference's exception text where one exists (e.g. ParseError "line N: ...", graph.hpp:17-26).
  *
+ * Limits (both fail loudly with VCG_EINVAL / VCG_ECUDA, never silently):
+ *   - dense engine (n <= 1024): per-worker node stacks of stack_bound records (greedy size, or
+ *     min(k, n)) of 16 + 64 W + 128 bytes, W = 4/8/16/32 words per row — C5 (n = 500, 3552
+ *     warps): 3552 x 484 x 1168 B = 2.0 GB;
+ *   - sparse engine (any n): u16 degrees, so every vertex degree must be < 65535; CSR offsets
+ *     are u32 on the device, so 2m < 2^32; the node's degree array sits in shared memory up to
+ *     about 110k vertices, in global memory beyond (the GDEG variant, engine 7); per-worker
+ *     scratch of 64 n bytes and node records of 16 + 2n bytes; a local stack deeper than its
+ *     device-memory cap hands its oldest node to the worklist, and only a full worklist then
+ *     ends the solve with an error.
+ *
  * Ownership: the caller owns every buffer it passes in (never retained beyond the call, except
  * that vcg_graph_* copy their inputs). The library owns vcg_graph objects (free with
  * vcg_graph_destroy) and the arrays inside a vcg_result (free with vcg_result_free). Device
@@ -112,8 +123,14 @@ typedef struct {
                                    2 sparse (any n, CTA per node),
                                    3 dense without renumbering (every node in the wide 32*W-slot
                                      layout; for A/B tests),
-                                   4 dense without the mid (<= 128 alive, per-warp frame) layout
-                                     (wide and compact only; for A/B tests) */
+                                   4 dense without the mid (per-warp frame) layout (wide and
+                                     compact only; for A/B tests),
+                                   5 / 6 dense with the mid layout forced to <= 256 / <= 128
+                                     alive vertices (n in 257..512; auto picks 256 for sparse
+                                     graphs, average degree < 24),
+                                   7 sparse with the node's degree array in global memory (the
+                                     variant auto picks when n is beyond the shared-memory limit,
+                                     about 110k vertices) */
     int32_t instrument;         /* 1: per-worker phase cycle counters */
     int32_t donate_oldest;      /* 1 (vcg_params_init's default): when donating, hand over the
                                    OLDEST stacked node (largest expected sub-tree) and stack the
@@ -138,14 +155,16 @@ typedef struct {
          (repeating on "yes"); reported as certify_nodes / certify_ms, within the caller's
          remaining timeout / node budget. A cross-check: the search is exact without it.
        VCG_DEBUG_CORRUPT_COVER — drop one vertex from the returned cover before verification
-         (tests the engine's own verify_cover check, which then fails with VCG_EVERIFY). */
+         (tests the engine's own verify_cover check, which then fails with VCG_EVERIFY).
+       VCG_DEBUG_SMALL_STACK — cap the sparse engine's local stacks at 3 nodes (tests the
+         hand-over of the oldest node to the worklist when a stack is full). */
     uint32_t debug_flags;
     /* Device workers (warps of the dense engine, CTAs of the sparse engine) to run. 0 = every
        SM filled (VCG_HYBRID) / `workers` (VCG_STACKONLY). Set it to run a fixed number, e.g.
        to give several shards on one device their share. */
     uint32_t device_workers;
 } vcg_params;
-enum { VCG_DEBUG_CERTIFY = 1, VCG_DEBUG_CORRUPT_COVER = 2 };
+enum { VCG_DEBUG_CERTIFY = 1, VCG_DEBUG_CORRUPT_COVER = 2, VCG_DEBUG_SMALL_STACK = 4 };
 
 typedef struct {
     int32_t status;             /* VCG_COMPLETE | VCG_TIMEOUT | VCG_BUDGET */

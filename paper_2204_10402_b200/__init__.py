@@ -190,7 +190,8 @@ def load_graph(path, fmt=None, complement_input=False) -> BaseGraph:
 _STRATEGIES = {"hybrid": _n.VCG_HYBRID, "gpu": _n.VCG_HYBRID, "seq": _n.VCG_SEQ,
                "stackonly": _n.VCG_STACKONLY}
 _RULES = {"reference": 0, "parallel": 1}
-_ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3, "dense-nomid": 4}
+_ENGINES = {"auto": 0, "dense": 1, "sparse": 2, "dense-wide": 3, "dense-nomid": 4,
+            "dense-mid8": 5, "dense-mid4": 6, "sparse-global": 7}
 
 
 def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, backoff_us,

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VCGPU_LIB", os.path.join(_HERE, "libvcgpu.so"))
 
 VCG_OK, VCG_EINVAL, VCG_EPARSE, VCG_ECUDA, VCG_ENOMEM, VCG_ERANGE, VCG_EVERIFY = range(7)
-VCG_DEBUG_CERTIFY, VCG_DEBUG_CORRUPT_COVER = 1, 2
+VCG_DEBUG_CERTIFY, VCG_DEBUG_CORRUPT_COVER, VCG_DEBUG_SMALL_STACK = 1, 2, 4
 VCG_MVC, VCG_PVC = 0, 1
 VCG_HYBRID, VCG_SEQ, VCG_STACKONLY = 0, 1, 2
 STATUS_NAMES = ("complete", "timeout", "budget")  # run_status_name (solver_seq.cpp:15-22)

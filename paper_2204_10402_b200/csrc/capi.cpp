@@ -249,6 +249,7 @@ struct HostRun {
         s.stack_bound = pvc ? std::min<uint32_t>(p->k, g.n) : greedy.size;
         s.seeds = p->seeds;
         s.num_seeds = p->num_seeds;
+        if (p->debug_flags & VCG_DEBUG_SMALL_STACK) s.stack_cap = 3;
         s.mailbox = p->mailbox;
         s.stream = p->stream;
     }
@@ -560,6 +561,7 @@ int vcg_expand_frontier(const vcg_graph* gh, const vcg_params* p, uint64_t targe
         s.k = p->k;
         s.device = p->device;
         s.stream = p->stream;
+        s.engine = p->engine;
         s.best = pvc ? p->k : greedy.size;
         if (!pvc && p->initial_best && p->initial_best < s.best) s.best = p->initial_best;
         vcg::Frontier f;

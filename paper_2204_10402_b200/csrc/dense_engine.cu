@@ -103,7 +103,7 @@ struct PinnedArena {
     }
 };
 struct DeviceCtx {
-    Arena stacks, wl, seq, misc, scratch;
+    Arena stacks, wl, seq, misc, scratch, gdeg;
     PinnedArena host;
     cudaStream_t stream = nullptr;
     cudaEvent_t evh = nullptr, ev0 = nullptr, ev1 = nullptr;
@@ -149,10 +149,11 @@ __global__ void gather_records_kernel(const unsigned char* src, const uint32_t* 
 // Dynamic shared memory of the dense kernels (dense_scratch_base / dense_degree_base): the
 // adjacency bitmap, a W-word slot per warp, W x 32 scratch words per warp, and with
 // VCG_WIDE_SMEM the wide degrees (W x 32 words per warp, laid out after 8 warps of scratch).
-size_t dense_smem_bytes(uint32_t W, uint32_t warps) {
+size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1) {
+    if (MW < 0) MW = default_mid((int)W);
     const size_t npad = 32 * (size_t)W;
     const size_t base = W * npad * 4 + 8 * (size_t)W * 4;
-    return VCG_WIDE_SMEM ? base + 8 * (size_t)W * 32 * 4 + warps * (size_t)W * 32 * 4
+    return VCG_WIDE_SMEM ? base + 8 * (size_t)W * 32 * 4 + warps * (size_t)dense_degree_words(W, MW) * 4
                          : base + warps * (size_t)W * 32 * 4;
 }
 
@@ -162,6 +163,11 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps) {
 #ifndef VCG_FLUSH_EVERY
 #define VCG_FLUSH_EVERY 64  // visits between a worker's node-counter flushes / limit checks
 #endif
+
+// average degree below which a W = 16 graph runs the <= 256-alive mid layout
+constexpr double kMid8MaxAvgDegree = 24.0;
+// edge density above which a W = 16 graph keeps the mid reduction out of line (see dense_kernel)
+constexpr double kMidOutOfLineDensity = 0.4;
 
 uint32_t pick_w(uint32_t n) {
     if (n <= 128) return 4;
@@ -206,24 +212,26 @@ void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint
         }
 }
 
-// Instantiations: (instrumented | plain) single-shard kernels, plus the plain multi-shard one.
-template <int W, bool INSTR>
+// Instantiations: (instrumented | plain) single-shard kernels, plus the plain multi-shard one;
+// W = 16 also with the wider mid layout (MW = 8, single-shard).
+template <int W, bool INSTR, int MW = default_mid(W), bool MOOL = false>
 void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s) {
     if (INSTR && a.world > 1)
         throw std::invalid_argument("instrumented runs are single-shard");
     auto k = a.world > 1 ? dense_kernel<W, false, true>
-             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true>
-                                            : dense_kernel<W, INSTR, false>;
+             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
+                                            : dense_kernel<W, INSTR, false, false, MW, MOOL>;
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, block, smem, s>>>(a);
     CUDA_CHECK(cudaGetLastError());
 }
 
-template <int W>
+template <int W, int MW = default_mid(W), bool MOOL = false>
 int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     int nb = 0;
     auto k = multi ? dense_kernel<W, false, true>
-                   : (instr ? dense_kernel<W, true, false> : dense_kernel<W, false, false>);
+                   : (instr ? dense_kernel<W, true, false, false, MW, MOOL>
+                            : dense_kernel<W, false, false, false, MW, MOOL>);
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)block, smem));
     return nb;
@@ -332,6 +340,8 @@ struct DenseRun {
     DeviceCtx& C;
     cudaStream_t st = nullptr;
     bool owned;  // own buffers and events (session) instead of the device arenas
+    bool mid8 = false;  // W = 16 kernel with the <= 256-alive mid layout
+    bool mool = false;  // W = 16 kernel with the mid reduction out of line (dense graphs)
     std::vector<void*> allocs;
     void* host = nullptr;
     size_t host_bytes = 0;
@@ -416,13 +426,24 @@ struct DenseRun {
         // worker grid: one warp per worker
         block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
         block = 32 * block_warps;
+        // The wider mid layout (<= 256 alive, 8 KB frames, 2 CTAs per SM) for sparse graphs,
+        // whose nodes keep a few hundred vertices alive (C2: 160-255); engine 5 forces it.
+        mid8 = W == 16 && !owned && s.engine != 3 && s.engine != 4 && s.engine != 6 &&
+               (s.engine == 5 || 2.0 * (double)g.m < kMid8MaxAvgDegree * (double)g.n);
+        // dense graphs (C5, C3: nearly every visit compact) keep the mid reduction out of line
+        mool = W == 16 && !owned && !mid8 &&
+               2.0 * (double)g.m > kMidOutOfLineDensity * (double)g.n * (double)(g.n - 1);
         // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-        smem = dense_smem_bytes(W, block_warps);
+        smem = dense_smem_bytes(W, block_warps, mid8 ? 8 : -1);
         int per_sm = 1;
         switch (W) {
             case 4: per_sm = occupancy<4>(block, smem, s.instrument, owned); break;
             case 8: per_sm = occupancy<8>(block, smem, s.instrument, owned); break;
-            case 16: per_sm = occupancy<16>(block, smem, s.instrument, owned); break;
+            case 16:
+                per_sm = mid8 ? occupancy<16, 8>(block, smem, s.instrument, owned)
+                              : mool ? occupancy<16, 4, true>(block, smem, s.instrument, owned)
+                                     : occupancy<16>(block, smem, s.instrument, owned);
+                break;
             default: per_sm = occupancy<32>(block, smem, s.instrument, owned); break;
         }
         if (per_sm < 1) throw std::runtime_error("CUDA error: dense kernel cannot be resident");
@@ -561,7 +582,11 @@ struct DenseRun {
         switch (W) {
             case 4: I ? launch_dense<4, true>(a, grid, block, smem, st) : launch_dense<4, false>(a, grid, block, smem, st); break;
             case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
-            case 16: I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st); break;
+            case 16:
+                if (mid8) I ? launch_dense<16, true, 8>(a, grid, block, smem, st) : launch_dense<16, false, 8>(a, grid, block, smem, st);
+                else if (mool) I ? launch_dense<16, true, 4, true>(a, grid, block, smem, st) : launch_dense<16, false, 4, true>(a, grid, block, smem, st);
+                else I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st);
+                break;
             default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
         }
         CUDA_CHECK(cudaEventRecord(ev1, st));
@@ -618,7 +643,7 @@ void check_dense_device(const Graph& g, const SolveSpec& s) {
 }  // namespace
 
 void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
-    if (s.engine == 2 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
+    if (s.engine == 2 || s.engine == 7 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
     check_dense_device(g, s);
     CUDA_CHECK(cudaSetDevice(s.device));
     DeviceCtx& C = ctx_for(s.device);
@@ -638,7 +663,7 @@ struct Session {
 };
 
 Session* session_open(const Graph& g, const SolveSpec& s) {
-    if (s.engine == 2 || g.n > 1024)
+    if (s.engine == 2 || s.engine == 7 || g.n > 1024)
         throw std::invalid_argument("multi-shard sessions need the dense engine (n <= 1024)");
     check_dense_device(g, s);
     if (s.strategy != 0) throw std::invalid_argument("multi-shard sessions run the hybrid strategies");
@@ -756,13 +781,12 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     if (maxdeg >= 0xFFFFu) throw std::invalid_argument("sparse engine: degree >= 65535");
     const uint32_t npad = (g.n + 7) / 8 * 8;
     const size_t entry = 16 + 2 * (size_t)npad;
-    const size_t smem = 2 * (size_t)npad + (2 * SP_THREADS + 1) * 4;
     int max_smem = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if (smem + sizeof(SpShared) + 1024 > (size_t)max_smem)
-        throw std::invalid_argument("graph has " + std::to_string(g.n) +
-                                    " vertices; the shared-memory degree array holds at most " +
-                                    std::to_string((max_smem - 12 * 1024) / 2));
+    // the degree array in shared memory when it fits, else in global memory (GDEG variant)
+    const size_t list_smem = (2 * SP_THREADS + 1) * 4;
+    const bool gdeg = s.engine == 7 || 2 * (size_t)npad + list_smem + sizeof(SpShared) + 1024 > (size_t)max_smem;
+    const size_t smem = (gdeg ? 0 : 2 * (size_t)npad) + list_smem;
     out.engine = 2;
     out.degree_bytes = 2;
     out.n_padded = npad;
@@ -799,11 +823,13 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     while (ring < cap) ring <<= 1;
     // per worker: 10n u32 lists, n u32 counters, n u64 claims, n u32 tags
     const size_t scratch_bytes = (size_t)workers * g.n * (12 * 4 + 4 + 8 + 4);
-    const size_t fixed = ring * entry + ring * 8 + scratch_bytes + (64ull << 20);
+    const size_t gdeg_bytes = gdeg ? (size_t)workers * npad * 2 : 0;
+    const size_t fixed = ring * entry + ring * 8 + scratch_bytes + gdeg_bytes + (64ull << 20);
     if (fixed >= free_b) throw std::runtime_error("CUDA error: out of device memory for the worklist");
     const uint64_t by_mem = (uint64_t)((free_b - fixed) * 0.6 / ((double)workers * entry));
     uint32_t bound = (uint32_t)std::min<uint64_t>((uint64_t)std::max<uint32_t>(s.stack_bound, 1) + 1,
                                                   std::max<uint64_t>(by_mem, 2));
+    if (s.stack_cap) bound = std::min(bound, s.stack_cap);
     unsigned char* stacks = (unsigned char*)C.stacks.get((size_t)workers * bound * entry);
     unsigned char* wl = (unsigned char*)C.wl.get(ring * entry);
     unsigned long long* seq = (unsigned long long*)C.seq.get(ring * 8);
@@ -822,6 +848,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     CUDA_CHECK(cudaMemsetAsync(cnt, 0, wn * 4, st));        // counters start at zero
     CUDA_CHECK(cudaMemsetAsync(owner, 0xFF, wn * 8, st));   // no triangle claims
     CUDA_CHECK(cudaMemsetAsync(tag, 0, wn * 4, st));        // epochs start at 1
+    uint16_t* gdeg_arr = gdeg ? (uint16_t*)C.gdeg.get(gdeg_bytes) : nullptr;
 
     // initial worklist: root (init_root) or the seeds, as u16 records
     const uint64_t nseeds = s.num_seeds ? s.num_seeds : 1;
@@ -890,15 +917,17 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     a.stackonly = s.strategy == 2 ? 1 : 0;
     a.depth = s.depth;
     a.mailbox = s.mailbox;
+    a.gdeg = gdeg_arr;
 
-    CUDA_CHECK(cudaFuncSetAttribute(sparse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = gdeg ? sparse_kernel<false, true> : sparse_kernel<false, false>;
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaEventRecord(C.ev0, st));
-    sparse_kernel<false><<<workers, SP_THREADS, smem, st>>>(a);
+    kern<<<workers, SP_THREADS, smem, st>>>(a);
     CUDA_CHECK(cudaGetLastError());
     const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
     if (hc.status == 3)
         throw std::runtime_error("CUDA error: search stack depth exceeded the device-memory cap (" +
-                                 std::to_string(bound) + " nodes per worker)");
+                                 std::to_string(bound) + " nodes per worker) with the worklist full");
     out.status = hc.status;
     out.wl_added = hc.tail;
     out.wl_current = (uint32_t)hc.work;
@@ -921,7 +950,172 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
 }
 
 
+namespace {
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            CUDA_CHECK(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return p;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+}  // namespace
+
+// The sparse engine's level-synchronous expansion (large n; sparse_expand_kernel): records are
+// sparse records (16 + 2 npad bytes), one CTA per node of a level.
+static void expand_frontier_sparse(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f) {
+    const int dev = s.device;
+    if (2 * g.m >= (1ull << 32)) throw std::invalid_argument("graph too large for u32 CSR offsets");
+    uint32_t maxdeg = 0;
+    for (uint32_t v = 0; v < g.n; ++v) maxdeg = std::max(maxdeg, g.degree(v));
+    if (maxdeg >= 0xFFFFu) throw std::invalid_argument("sparse engine: degree >= 65535");
+    CUDA_CHECK(cudaSetDevice(dev));
+    DeviceCtx& C = ctx_for(dev);
+    std::lock_guard<std::mutex> solve_lock(C.solve_mu);
+    cudaStream_t st = s.stream ? static_cast<cudaStream_t>(s.stream) : C.stream;
+    const uint32_t npad = (g.n + 7) / 8 * 8;
+    const size_t entry = 16 + 2 * (size_t)npad;
+    int max_smem = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t list_smem = (2 * SP_THREADS + 1) * 4;
+    const bool gdeg = s.engine == 7 || 2 * (size_t)npad + list_smem + sizeof(SpShared) + 1024 > (size_t)max_smem;
+    const size_t smem = (gdeg ? 0 : 2 * (size_t)npad) + list_smem;
+    if ((int)g.dev.size() <= dev) g.dev.resize(dev + 1);
+    if (!g.dev[dev] || !g.dev[dev]->off) {
+        auto dg = g.dev[dev] ? g.dev[dev] : std::make_shared<DeviceGraph>();
+        dg->device = dev;
+        std::vector<uint32_t> off32(g.n + 1);
+        for (uint32_t v = 0; v <= g.n; ++v) off32[v] = (uint32_t)g.off[v];
+        CUDA_CHECK(cudaMalloc(&dg->off, off32.size() * 4));
+        CUDA_CHECK(cudaMalloc(&dg->nbr, std::max<size_t>(1, g.nbr.size()) * 4));
+        CUDA_CHECK(cudaMemcpy(dg->off, off32.data(), off32.size() * 4, cudaMemcpyHostToDevice));
+        if (!g.nbr.empty())
+            CUDA_CHECK(cudaMemcpy(dg->nbr, g.nbr.data(), g.nbr.size() * 4, cudaMemcpyHostToDevice));
+        dg->csr_bytes = off32.size() * 4 + g.nbr.size() * 4;
+        g.dev[dev] = dg;
+    }
+    const DeviceGraph& dg = *g.dev[dev];
+    const uint32_t ctas = (uint32_t)C.sms;
+    const size_t wn = (size_t)ctas * g.n;
+    const uint32_t cover_words = (g.n + 31) / 32;
+    DevBuf bin, bout, bflags, bcov, bidx, bscr, bgdeg;
+    unsigned char* scr = (unsigned char*)bscr.get(wn * (12 * 4 + 4 + 8 + 4));
+    SparseExpandArgs e{};
+    SparseArgs& a = e.s;
+    a.off = dg.off;
+    a.nbr = dg.nbr;
+    a.n = g.n;
+    a.npad = npad;
+    a.pvc = s.pvc ? 1 : 0;
+    a.k = s.k;
+    a.entry_bytes = entry;
+    a.cover_words = cover_words;
+    a.owner = reinterpret_cast<unsigned long long*>(scr);
+    a.scratch = reinterpret_cast<uint32_t*>(scr + wn * 8);
+    a.cnt = reinterpret_cast<uint32_t*>(scr + wn * 56);
+    a.tag = reinterpret_cast<uint32_t*>(scr + wn * 60);
+    a.gdeg = gdeg ? (uint16_t*)bgdeg.get((size_t)ctas * npad * 2) : nullptr;
+    {
+        std::vector<unsigned char> root(entry, 0);
+        uint32_t* h = reinterpret_cast<uint32_t*>(root.data());
+        uint16_t* dd = reinterpret_cast<uint16_t*>(root.data() + 16);
+        h[0] = 0;
+        h[1] = (uint32_t)g.m;
+        for (uint32_t v = 0; v < npad; ++v) dd[v] = v < g.n ? (uint16_t)g.degree(v) : DREM;
+        CUDA_CHECK(cudaMemcpyAsync(bin.get(entry), root.data(), entry, cudaMemcpyHostToDevice, st));
+    }
+    auto kern = gdeg ? sparse_expand_kernel<true> : sparse_expand_kernel<false>;
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    uint64_t count = 1;
+    f = Frontier();
+    f.best = s.best;
+    std::vector<uint32_t> flags, covers, idx;
+    while (count > 0 && count < target) {
+        // fresh claim / tag / counter state per level (epochs restart with every launch)
+        CUDA_CHECK(cudaMemsetAsync(a.owner, 0xFF, wn * 8, st));
+        CUDA_CHECK(cudaMemsetAsync(a.cnt, 0, wn * 4, st));
+        CUDA_CHECK(cudaMemsetAsync(a.tag, 0, wn * 4, st));
+        e.in = (unsigned char*)bin.p;
+        e.out = (unsigned char*)bout.get(2 * count * entry);
+        e.flags = (uint32_t*)bflags.get(count * 4);
+        e.covers = (uint32_t*)bcov.get(count * (cover_words + 1) * 4);
+        e.count = (uint32_t)count;
+        e.best = f.best;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(count, ctas);
+        kern<<<grid, SP_THREADS, smem, st>>>(e);
+        CUDA_CHECK(cudaGetLastError());
+        ++f.launches;
+        flags.resize(count);
+        CUDA_CHECK(cudaMemcpyAsync(flags.data(), e.flags, count * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        f.nodes += count;
+        ++f.levels;
+        bool any_cover = false;
+        for (uint64_t i = 0; i < count; ++i) any_cover |= flags[i] == 1;
+        if (any_cover) {
+            covers.resize(count * (cover_words + 1));
+            CUDA_CHECK(cudaMemcpy(covers.data(), e.covers, covers.size() * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < count; ++i) {
+                if (flags[i] != 1) continue;
+                const uint32_t* c = &covers[i * (cover_words + 1)];
+                if (s.pvc ? !f.found : c[0] < f.best) {
+                    f.found = true;
+                    if (!s.pvc) f.best = c[0];
+                    f.cover.clear();
+                    for (uint32_t v = 0; v < g.n; ++v)
+                        if ((c[1 + (v >> 5)] >> (v & 31)) & 1u) f.cover.push_back(v);
+                }
+            }
+        }
+        if (s.pvc && f.found) {
+            count = 0;
+            break;
+        }
+        idx.clear();
+        for (uint64_t i = 0; i < count; ++i)
+            if (flags[i] == 2) {
+                idx.push_back((uint32_t)(2 * i));
+                idx.push_back((uint32_t)(2 * i + 1));
+            }
+        const uint64_t nc = idx.size();
+        if (nc) {
+            uint32_t* didx = (uint32_t*)bidx.get(nc * 4);
+            CUDA_CHECK(cudaMemcpyAsync(didx, idx.data(), nc * 4, cudaMemcpyHostToDevice, st));
+            unsigned char* dnext = (unsigned char*)bin.get(nc * entry);
+            gather_records_kernel<<<(uint32_t)std::min<uint64_t>(nc, 65535), 256, 0, st>>>(
+                e.out, didx, dnext, (uint32_t)nc, (uint32_t)(entry / 16));
+            CUDA_CHECK(cudaGetLastError());
+            ++f.launches;
+        }
+        count = nc;
+    }
+    std::vector<unsigned char> level(count * entry);
+    if (count) {
+        CUDA_CHECK(cudaMemcpyAsync(level.data(), bin.p, count * entry, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    f.records.assign(count * (2 + (size_t)g.n), 0);
+    for (uint64_t i = 0; i < count; ++i) {
+        const unsigned char* rec = level.data() + i * entry;
+        uint32_t* r = f.records.data() + i * (2 + (size_t)g.n);
+        r[0] = reinterpret_cast<const uint32_t*>(rec)[0];
+        r[1] = reinterpret_cast<const uint32_t*>(rec)[1];
+        const uint16_t* dd = reinterpret_cast<const uint16_t*>(rec + 16);
+        for (uint32_t v = 0; v < g.n; ++v) r[2 + v] = dd[v] == DREM ? REM : dd[v];
+    }
+    f.count = count;
+}
+
 void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f) {
+    if (s.engine == 2 || s.engine == 7 || g.n > 1024) return expand_frontier_sparse(g, s, target, f);
     if (g.n > 1024)
         throw std::invalid_argument("frontier expansion needs the dense engine (n <= 1024)");
     const int dev = s.device;
@@ -950,22 +1144,7 @@ void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Fronti
 
     // Levels stay on the device: per level only the flags come down and the gather list of
     // surviving children goes up; the final level is copied once.
-    struct DevBuf {
-        void* p = nullptr;
-        size_t bytes = 0;
-        void* get(size_t need) {
-            if (need > bytes) {
-                if (p) cudaFree(p);
-                p = nullptr;
-                CUDA_CHECK(cudaMalloc(&p, need));
-                bytes = need;
-            }
-            return p;
-        }
-        ~DevBuf() {
-            if (p) cudaFree(p);
-        }
-    } bin, bout, bflags, bcov, bidx;
+    DevBuf bin, bout, bflags, bcov, bidx;
     {
         std::vector<unsigned char> root(entry);
         std::vector<uint32_t> deg(g.n);

@@ -303,10 +303,18 @@ template <int W>
 __device__ __forceinline__ uint32_t dense_scratch_base(uint32_t wib) {
     return (W / 4) * (32 * W) * 4 + 8 * W + wib * W * 32;
 }
-// (VCG_WIDE_SMEM) per-warp degree words after the scratch words of 8 warps
-template <int W>
+// (VCG_WIDE_SMEM) per-warp degree words after the scratch words of 8 warps; with a mid layout
+// of width MW the region also holds the warp's frame bitmap ([MW/4][32 MW] uint4), which
+// overlays the wide degrees (a warp holds one current node).
+__host__ __device__ constexpr uint32_t dense_degree_words(int W, int MW) {
+    return (uint32_t)W * 32 > (uint32_t)(MW / 4) * (32 * MW) * 4 ? (uint32_t)W * 32
+                                                                  : (uint32_t)(MW / 4) * (32 * MW) * 4;
+}
+// the mid width of the default instantiation: 4 (<= 128 alive) where the graph is >= 16 words
+__host__ __device__ constexpr int default_mid(int W) { return W >= 16 ? 4 : 0; }
+template <int W, int MW = default_mid(W)>
 __device__ __forceinline__ uint32_t dense_degree_base(uint32_t wib) {
-    return dense_scratch_base<W>(8) + wib * W * 32;
+    return dense_scratch_base<W>(8) + wib * dense_degree_words(W, MW);
 }
 
 // WG == 0: the WIDE layout over the whole graph (vertex v at lane v & 31, word v >> 5). WG != 0:
@@ -1347,7 +1355,7 @@ __device__ __noinline__ bool record_cover_(Ctl* ctl, uint32_t* cover_slots, vola
 
 enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
 
-template <int W, bool INSTR, bool MULTI, bool ONEW = false>
+template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid(W), bool MOOL = false>
 #ifndef VCG_MINB16
 #define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
 #endif               // (wide degrees in smem: 3 → 80 regs, C5 10.2 ms; 2 → 127 regs, 10.8 ms; 4 → 64 + spills, 12.9)
@@ -1358,7 +1366,12 @@ template <int W, bool INSTR, bool MULTI, bool ONEW = false>
 #define VCG_MINB_MULTI 2  // the multi-shard instantiation (W = 16): 128 registers, no spills
                           // (2 shards on one B200: 14.1 ms vs 16.0 ms at 3 CTAs/SM with spills)
 #endif
-__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : VCG_MINB16) : 1))) dense_kernel(DenseArgs a) {
+// MW: the mid layout's width (0 none, 4: <= 128 alive, 8: <= 256 alive — its 8 KB frames leave
+// room for 2 CTAs per SM; for sparse graphs whose nodes stay wide). MOOL: the mid reduction out
+// of line — for dense graphs, whose visits are nearly all compact: inlined, the third copy of the
+// rule code costs the compact hot loop registers and instruction cache (C5 9.7 -> 11.9 ms),
+// while out of line the mid node's register degrees go through local memory around the call.
+__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : (MW == 8 ? 2 : VCG_MINB16)) : 1))) dense_kernel(DenseArgs a) {
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -1375,7 +1388,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     unsigned long long* const t0s = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
     // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
-    constexpr int MW = W >= 16 ? 4 : 0;  // mid layout width (words per frame row)
+    static_assert(MW == 0 || (W >= 16 && (MW == 4 || MW == 8)), "mid layout width");
     if (lane == 0) {
         t0s[0] = globaltimer();
         t0s[1] = (unsigned long long)clock64();
@@ -1392,7 +1405,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     WarpNode<W, INSTR> x;
     x.ssb = dense_scratch_base<W>(wib);
 #if VCG_WIDE_SMEM
-    x.dsb = dense_degree_base<W>(wib);
+    x.dsb = dense_degree_base<W, MW>(wib);
 #endif
     x.lane = lane;
     CompactNode<INSTR> y;
@@ -1402,7 +1415,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     WarpNode<MW ? MW : 4, INSTR, W> m;
     m.lane = lane;
     m.ssb = x.ssb;
-    m.rb = dense_degree_base<W>(wib) / 4;
+    m.rb = dense_degree_base<W, MW>(wib) / 4;
     m.idb = (x.ssb + (MW ? MW : 4) * 32) * 2;
     m.tgi = (uint32_t)(reinterpret_cast<uint32_t*>(t0s) - reinterpret_cast<uint32_t*>(dense_smem)) / 2 + 2;
     enum { M_WIDE = 0, M_COMPACT = 1, M_MID = 2 };
@@ -1447,7 +1460,11 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto reduce_under_B = [&](auto& n) {
         using NT = typename std::remove_reference<decltype(n)>::type;
-        if constexpr (VCG_WIDE_NOINLINE && !INSTR && !std::is_same<NT, CompactNode<INSTR>>::value) {
+        // (only the wide layout out of line: its degrees are in shared memory anyway, while a
+        // call taking the mid node by reference would move its register degrees to local memory)
+        if constexpr (VCG_WIDE_NOINLINE && !INSTR &&
+                      (std::is_same<NT, WarpNode<W, INSTR>>::value ||
+                       (MOOL && !std::is_same<NT, CompactNode<INSTR>>::value))) {
             const RuleDeltas dl = wide_reduce(n, B);
             st.rounds += dl.rounds;
             st.rm1 += dl.rm1;

@@ -33,6 +33,7 @@ struct SolveSpec {
     volatile uint32_t* mailbox = nullptr;
     void* stream = nullptr;     // caller's cudaStream_t (null: the library's stream)
     bool no_root = false;       // multi-shard: no seeds means an empty worklist, not the root
+    uint32_t stack_cap = 0;     // debug (VCG_DEBUG_SMALL_STACK): cap the sparse local stack
 };
 
 struct SolveOut {

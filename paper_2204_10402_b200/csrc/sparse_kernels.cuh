@@ -58,6 +58,7 @@ struct SparseArgs {
     int stackonly;            // StackOnly strategy (scheduler.cpp:214-297)
     uint32_t depth;
     volatile uint32_t* mailbox;
+    uint16_t* gdeg;           // GDEG kernels: workers * npad u16 degree arrays in global memory
 };
 
 // CTA-wide shared control block (decisions are made here and read after a barrier)
@@ -546,6 +547,14 @@ struct CtaNode {
         fresh = false;
         __syncthreads();
     }
+    // the current node as a record {cc, edges, 0, 0} + u16 degrees
+    __device__ void store_current(unsigned char* rec) const {
+        const uint4* s4 = reinterpret_cast<const uint4*>(deg);
+        uint4* d4 = reinterpret_cast<uint4*>(rec + 16);
+        for (uint32_t i = threadIdx.x; i < a->npad / 8; i += SP_THREADS) d4[i] = s4[i];
+        if (threadIdx.x == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(sh->cc, sh->edges, 0u, 0u);
+        __syncthreads();
+    }
     __device__ void copy_record(const unsigned char* src, unsigned char* dst) const {
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
         uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -637,17 +646,17 @@ struct CtaNode {
     }
 };
 
-template <bool INSTR>
-__global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
-    extern __shared__ uint4 smem4[];
-    __shared__ SpShared sh;
-    const uint32_t worker = blockIdx.x;
-    if (worker >= a.workers) return;
-    const int tid = threadIdx.x;
-
-    CtaNode x;
-    x.deg = reinterpret_cast<uint16_t*>(smem4);
-    x.cbuf = reinterpret_cast<uint32_t*>(x.deg + a.npad);
+// One CTA's node and its per-worker scratch (lists in global memory, claims, tags, counters).
+template <bool GDEG>
+__device__ __forceinline__ void init_cta_node(CtaNode& x, const SparseArgs& a, uint32_t worker,
+                                              uint4* smem4, SpShared& sh) {
+    if constexpr (GDEG) {
+        x.deg = a.gdeg + (unsigned long long)worker * a.npad;
+        x.cbuf = reinterpret_cast<uint32_t*>(smem4);
+    } else {
+        x.deg = reinterpret_cast<uint16_t*>(smem4);
+        x.cbuf = reinterpret_cast<uint32_t*>(x.deg + a.npad);
+    }
     x.cstart = x.cbuf + SP_THREADS;
     x.sh = &sh;
     x.a = &a;
@@ -667,6 +676,21 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
     x.tag = a.tag + (unsigned long long)worker * a.n;
     x.epoch = 0;
     x.fresh = false;
+}
+
+// GDEG: the global-memory node variant for graphs whose degree array does not
+// fit in shared memory (n beyond ~110k): the current node's u16 degrees live in a per-worker
+// array in global memory (L2-resident: 148 workers x 2n bytes), everything else is unchanged.
+template <bool INSTR, bool GDEG = false>
+__global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
+    extern __shared__ uint4 smem4[];
+    __shared__ SpShared sh;
+    const uint32_t worker = blockIdx.x;
+    if (worker >= a.workers) return;
+    const int tid = threadIdx.x;
+
+    CtaNode x;
+    init_cta_node<GDEG>(x, a, worker, smem4, sh);
     if (tid == 0) sh.ecut = 0;
 
     const unsigned long long t_start = globaltimer();
@@ -859,8 +883,37 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         const bool right = replaying && ((subtree >> replay) & 1ull);
         replay += replaying;
         if (!replaying || right) {
+            if (!child && sp >= a.stack_bound && !a.seq_mode) {
+                // The local stack reached its device-memory cap: its oldest node moves to the
+                // device worklist (the shared HBM pool), whatever the donation threshold.
+                if (tid == 0) {
+                    int ok = 0;
+                    const unsigned long long old = atomicAdd(&ctl->work, ONE_PENDING | 1ull);
+                    if ((uint32_t)old >= a.capacity) {
+                        atomicAdd(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
+                    } else {
+                        sh.pos = atomicAdd(&ctl->tail, 1ull);
+                        ok = 1;
+                        if (ld_acquire_u64(a.seq + (sh.pos & a.ring_mask)) != sh.pos)
+                            ok = wait_slot_free(a.seq + (sh.pos & a.ring_mask), sh.pos, &ctl->cancel, false) ? 1 : 2;
+                    }
+                    sh.outcome = ok;
+                }
+                __syncthreads();
+                const int ok = sh.outcome;
+                if (ok == 1) {
+                    const unsigned long long p2 = sh.pos;
+                    x.copy_record(slot_at(0), a.wl + (p2 & a.ring_mask) * a.entry_bytes);
+                    base = base + 1 == a.stack_bound ? 0 : base + 1;
+                    --sp;
+                    ++st.donated;
+                    __threadfence();
+                    __syncthreads();
+                    if (tid == 0) st_release_u64(a.seq + (p2 & a.ring_mask), p2 + 1);
+                }
+            }
             if (!child) {
-                if (sp >= a.stack_bound) {  // deeper than the device-memory cap: fail loudly
+                if (sp >= a.stack_bound) {  // the worklist is full too: fail loudly
                     if (tid == 0) {
                         atomicCAS(&ctl->status, 0, 3);
                         atomicExch(&ctl->cancel, 1u);
@@ -907,6 +960,60 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         for (int p = 0; p < 10; ++p) o.phase[p] = 0;
         a.stats[worker] = o;
         (void)t_start;
+    }
+}
+
+// Level-synchronous frontier expansion on the sparse engine (multi-GPU partitioning for large
+// n): CTA i processes node i of a level exactly as process_node does
+// (scheduler.cpp:125-144) with a FIXED bound, writes its remove-N(v) child to out[2i] and its
+// remove-v child to out[2i+1]. The block-parallel rules reach the same fixpoint whatever the
+// thread schedule, so every rank derives the same frontier.
+struct SparseExpandArgs {
+    SparseArgs s;             // graph, scratch (gridDim.x workers), gdeg
+    const unsigned char* in;
+    unsigned char* out;
+    uint32_t* flags;          // per input: 0 pruned, 1 cover found, 2 branched
+    uint32_t* covers;         // per input: [cc, bitmap cover_words]
+    uint32_t count, best;
+};
+
+template <bool GDEG>
+__global__ void __launch_bounds__(SP_THREADS, 1) sparse_expand_kernel(SparseExpandArgs e) {
+    extern __shared__ uint4 smem4[];
+    __shared__ SpShared sh;
+    const SparseArgs& a = e.s;
+    CtaNode x;
+    init_cta_node<GDEG>(x, a, blockIdx.x, smem4, sh);
+    if (threadIdx.x == 0) sh.ecut = 0;
+    Counters st;
+    for (uint32_t i = blockIdx.x; i < e.count; i += gridDim.x) {
+        x.load_record(e.in + (unsigned long long)i * a.entry_bytes);
+        x.reduce(e.best, st);
+        uint32_t flag;
+        if (sh.doom || should_prune(a.pvc, a.k, e.best, sh.cc, sh.edges)) {
+            flag = 0;
+        } else if (sh.edges == 0) {
+            flag = 1;
+            uint32_t* c = e.covers + (unsigned long long)i * (a.cover_words + 1);
+            for (uint32_t w = threadIdx.x; w < a.cover_words; w += SP_THREADS) {
+                uint32_t bits = 0;
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t v = 32 * w + j;
+                    if (v < a.n && x.deg[v] == DREM) bits |= 1u << j;
+                }
+                c[1 + w] = bits;
+            }
+            if (threadIdx.x == 0) c[0] = sh.cc;
+        } else {
+            flag = 2;
+            x.scan(0xFFFFu, false);
+            const uint32_t v = 0xFFFFFFFFu - (uint32_t)(sh.maxkey & 0xFFFFFFFFull);
+            x.write_child(v, e.out + (2ull * i) * a.entry_bytes);
+            x.remove_branch_vertex(v);
+            x.store_current(e.out + (2ull * i + 1) * a.entry_bytes);
+        }
+        if (threadIdx.x == 0) e.flags[i] = flag;
+        __syncthreads();
     }
 }
 

@@ -65,11 +65,15 @@ class Mailbox:
             pass
 
 
-def expand_frontier(graph, mode, k, target, device=0, stream=None, initial_best=0):
+def expand_frontier(graph, mode, k, target, device=0, stream=None, initial_best=0, engine="auto"):
     """Deterministic device expansion (vcg_expand_frontier) → dict with ``seeds`` as an
-    (count, 2 + n) uint32 array of [cover_count, edge_count, degrees...] records."""
+    (count, 2 + n) uint32 array of [cover_count, edge_count, degrees...] records. Graphs beyond
+    the dense engine (n > 1024, or engine "sparse") expand on the sparse engine, one CTA per
+    node of a level."""
+    from . import _ENGINES
     p = _n.Params()
     _lib.vcg_params_init(C.byref(p))
+    p.engine = _ENGINES[engine]
     p.mode = _n.VCG_PVC if mode == "pvc" else _n.VCG_MVC
     p.k = k
     p.device = device
@@ -154,6 +158,8 @@ def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_p
     import torch.distributed as dist
     if mode == "pvc" and k < 1:
         raise ValueError("pvc requires k >= 1")
+    if exchange == "peer" and graph.num_vertices > 1024:
+        exchange = "host"  # linked device worklists are dense-engine shards; large n: static shares
     if exchange == "peer" and solver is None:
         return _solve_peer(graph, mode, k, exchange_group, frontier_per_rank, device,
                            expander or expand_frontier, shard_factory, solve_kw)
@@ -168,7 +174,8 @@ def solve_distributed(graph, mode="pvc", k=0, *, exchange_group=None, frontier_p
             return (solve_pvc(g, k, raw=True, **kw) if pvc else solve_mvc(g, raw=True, **kw))
 
     t0 = time.perf_counter()
-    fr = expander(graph, mode, k, frontier_per_rank * world, device=device, stream=stream)
+    fr = expander(graph, mode, k, frontier_per_rank * world, device=device, stream=stream,
+                  **({"engine": solve_kw["engine"]} if "engine" in solve_kw else {}))
     share = fr["seeds"][rank::world]
     decided = pvc and fr["found"]
     res = _empty_result(graph, pvc)

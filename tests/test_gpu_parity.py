@@ -554,3 +554,134 @@ def test_c2_pvc_yes_at_k241(config_golden):
     assert r["status"] == "complete" and r["feasible"]
     assert r["size"] <= 241
     check_cover(g, r)
+
+
+# ---- mid layout (per-warp frame renumbering, <= 128 / <= 256 alive) ------------------------
+
+@pytest.mark.parametrize("engine", ["dense-mid4", "dense-mid8", "dense-nomid"])
+def test_mid_layouts_visit_the_reference_tree(config_golden, engine):
+    """The frame renumbering keeps the id order: PVC no-instance node counts equal the
+    reference's, and the 1-warp seq order is the reference's node for node (C3, n = 300: the
+    mid layouts act on nodes with 65-256 alive vertices)."""
+    for name in ("c3", "c5"):
+        g = load_config(name)
+        gold = config_golden[name]
+        r = vc.solve_pvc(g, gold["pvc_no_k"], strategy="gpu", engine=engine)
+        assert not r["feasible"] and r["nodes_total"] == gold["pvc_no_nodes"], (name, r["nodes_total"])
+    g = load_config("c3")
+    s = vc.solve_mvc(g, strategy="seq", engine=engine)
+    assert s["size"] == config_golden["c3"]["mvc"]
+    assert sum(s["worker_nodes"]) == config_golden["c3"]["seq_nodes"]
+
+
+@pytest.mark.parametrize("n,deg,seed", [(300, 3.0, 3), (400, 3.0, 4), (500, 2.5, 5)])
+def test_mid_layouts_on_sparse_graphs_against_the_oracle(oracle, n, deg, seed):
+    """Sparse W = 16 graphs (nodes keep 100-300 vertices alive: the <= 256 frame, rebuilt on
+    donated records): MVC, the PVC no-instance node count and the seq order equal the oracle's."""
+    from oracle.oracle import CSR
+    rng = np.random.default_rng(seed)
+    iu = np.triu_indices(n, 1)
+    keep = rng.random(len(iu[0])) < deg / (n - 1)
+    g = vc.make_graph(n, list(zip(iu[0][keep].tolist(), iu[1][keep].tolist())))
+    off, nbr = g.csr()
+    csr = CSR(n, g.num_edges, off, nbr)
+    want = oracle.solve_seq(csr, node_budget=3_000_000)
+    if want["status"] != "complete":
+        pytest.skip("oracle budget")
+    no = oracle.solve_seq(csr, pvc=True, k=want["size"] - 1, node_budget=6_000_000)
+    for engine in ("auto", "dense-mid8", "dense-mid4"):
+        r = vc.solve_mvc(g, strategy="gpu", engine=engine)
+        assert r["size"] == want["size"], engine
+        check_cover(g, r)
+        if no["status"] == "complete":
+            p = vc.solve_pvc(g, want["size"] - 1, strategy="gpu", engine=engine)
+            assert not p["feasible"] and p["nodes_total"] == no["nodes"], (engine, p["nodes_total"])
+    s = vc.solve_mvc(g, strategy="seq", engine="dense-mid8")
+    assert s["size"] == want["size"] and sum(s["worker_nodes"]) == want["nodes"]
+
+
+# ---- large n: the global-memory node variant, stack overflow, sparse frontier --------------
+
+def _ba_edges(n, m, seed):
+    """Barabasi-Albert preferential attachment (each new vertex picks m distinct targets,
+    proportionally to degree, by sampling the endpoint list)."""
+    rng = np.random.default_rng(seed)
+    ends = list(range(m))
+    edges = []
+    for v in range(m, n):
+        chosen = set()
+        while len(chosen) < m:
+            chosen.add(ends[int(rng.integers(len(ends)))] if len(ends) > m else int(rng.integers(v)))
+        for u in chosen:
+            edges.append((u, v))
+            ends.extend((u, v))
+    return edges
+
+
+def test_sparse_global_variant_corpus_exact(corpus):
+    """engine="sparse-global" (degree array in global memory): exact on the corpus."""
+    bad = []
+    for it in corpus[::3]:
+        g = graph_of(it)
+        r = vc.solve_mvc(g, strategy="gpu", engine="sparse-global")
+        check_cover(g, r)
+        if r["size"] != it["mvc"] or r["status"] != "complete" or r["engine"] != 2:
+            bad.append((it["name"], r["size"], it["mvc"]))
+    assert not bad, bad[:10]
+
+
+def test_large_n_ba300k_budgeted_run():
+    """n = 300k is beyond the shared-memory degree array: the global-memory variant runs it."""
+    n = 300_000
+    g = vc.make_graph(n, _ba_edges(n, 3, 7))
+    r = vc.solve_mvc(g, strategy="gpu", node_budget=3000)
+    assert r["engine"] == 2 and r["status"] == "budget" and r["nodes_total"] >= 3000
+    assert r["size"] <= r["greedy_size"]
+    check_cover(g, r)
+
+
+def test_sparse_stack_overflow_hands_nodes_to_the_worklist(corpus, config_golden):
+    """Local stacks capped at 3 nodes (debug): full stacks hand their oldest node to the
+    worklist instead of failing, and the answers stay exact."""
+    bad = []
+    for it in corpus[::4]:
+        g = graph_of(it)
+        r = vc.solve_mvc(g, strategy="gpu", engine="sparse", debug_flags=vc._n.VCG_DEBUG_SMALL_STACK)
+        if r["size"] != it["mvc"] or r["status"] != "complete":
+            bad.append((it["name"], r["size"], it["mvc"]))
+    assert not bad, bad[:10]
+    g = load_config("c3")
+    r = vc.solve_mvc(g, strategy="gpu", engine="sparse", debug_flags=vc._n.VCG_DEBUG_SMALL_STACK)
+    assert r["size"] == config_golden["c3"]["mvc"]
+    check_cover(g, r)
+
+
+def test_sparse_frontier_expansion_partitions_exactly(oracle):
+    """vcg_expand_frontier on the sparse engine (n > 1024): the frontier shares, solved
+    separately, give the direct solve's optimum (a two-rank partition in one process)."""
+    from oracle.oracle import CSR
+    from paper_2204_10402_b200.distributed import expand_frontier
+    rng = np.random.default_rng(11)
+    n = 1500
+    edges = _random_tree(n, 11) + [tuple(map(int, rng.integers(0, n, 2))) for _ in range(160)]
+    g = vc.make_graph(n, edges)
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(n, g.num_edges, off, nbr), node_budget=5_000_000)
+    assert want["status"] == "complete"
+    fr = expand_frontier(g, "mvc", 0, 16)
+    assert fr["nodes"] >= 1 and fr["levels"] >= 1
+    best = fr["best"]
+    sizes = [len(fr["cover"])]
+    for rank in range(2):
+        share = fr["seeds"][rank::2]
+        if len(share):
+            r = vc.solve_mvc(g, strategy="gpu", seeds=share, initial_best=best)
+            check_cover(g, r)
+            if r["cover_from_search"]:
+                sizes.append(r["size"])
+    assert min(sizes) == want["size"]
+    # C4 (n = 100k): the expansion itself on the large config
+    c4 = load_config("c4")
+    f4 = expand_frontier(c4, "mvc", 0, 32)
+    assert len(f4["seeds"]) >= 32 or f4["found"]
+    assert f4["seeds"].shape[1] == c4.num_vertices + 2
