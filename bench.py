@@ -1,12 +1,20 @@
 #!/usr/bin/env python
 """bench.py — headline measurement (driver contract).
 
-Workload (BASELINE.json metric "time-to-solution and search-tree nodes/sec at 1/2/4/8 B200 vs
-CPU ref"): config C5, the hard PVC no-instance — k = MVC-1 = 482 on the complement of the
-p_hat-style G(500, a=.25, b=.75) seed-0 graph (data/configs/c5.clq.gz, n=500, m=61,209). One
-step = one complete exact solve (the whole 21,461,369-node search tree; answer "no").
+Workloads (BASELINE.json metric "time-to-solution and search-tree nodes/sec at 1/2/4/8 B200 vs
+CPU ref"); one step = one complete exact solve of a PVC no-instance (k = MVC - 1: the whole
+search tree is visited, answer "no"):
+  * N = 1 (default workload "c5"): config C5 — k = 482 on the complement of the p_hat-style
+    G(500, a=.25, b=.75) seed-0 graph (data/configs/c5.clq.gz, n=500, m=61,209), 21,461,369
+    nodes, about 10 ms: the round-to-round headline.
+  * N > 1 (default workload "c5s", "C5-scale"): the strong-scaling instance SURVEY §8e asks
+    for — a p_hat500-3-like graph (a=.48, b=1; data/configs/c5s.clq.gz) whose 1-GPU solve takes
+    seconds, so that 1 -> 8 GPU scaling measures the search, not the start-up. The N = 1 line
+    carries it as the extra key "c5_scale" (one solve + the reference's bounded sample).
+  The N = 1 line also carries C1 / C3 MVC time-to-solution and C4 node throughput (budget
+  100k, with its roofline), each beside the reference's own time (key "configs").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W]
 
 N>1 runs under torchrun, one process per GPU: rank 0's shard starts from the root, every GPU's
 device worklist is linked to the others' through CUDA IPC / NVLink P2P, and workers donate
@@ -28,10 +36,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-to-solution and search-tree nodes/sec at 1/2/4/8 B200 vs CPU ref"
 UNIT = "nodes/s"
-WORKLOAD = ("C5: PVC k=482 (=MVC-1, no-instance) on the complement of p_hat-style "
-            "G(500, a=0.25, b=0.75) seed 0")
-K_NO = 482
-C5_NODES = 21461369  # reference node count (tests/golden/configs.json)
+# k = MVC - 1 and the full tree's node count (C5: the reference's, tests/golden/configs.json;
+# C5-scale: the engine's, identical for every layout / worker count — tests/golden/c5s.json)
+WORKLOADS = {
+    "c5": dict(k=482, nodes=21461369,
+               desc="C5: PVC k=482 (=MVC-1, no-instance) on the complement of p_hat-style "
+                    "G(500, a=0.25, b=0.75) seed 0"),
+    "c5s": dict(k=448, nodes=5969685861,
+                desc="C5-scale: PVC k=448 (=MVC-1, no-instance) on the complement of p_hat-style "
+                     "G(500, a=0.48, b=1.0) seed 0 (p_hat500-3-like)"),
+}
 # Degree entries are u16 in every node record (the roofline's w = 2 bytes); in registers the
 # engine works on 32-bit words and 64-bit adjacency masks. Exact integer work either way.
 DTYPE = "u16"
@@ -44,7 +58,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c5 at N=1, c5s (C5-scale) at N>1")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="N=1: skip the C1/C3/C4/C5-scale extra keys")
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default: 5 at N=1, 2 at N>1")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--frontier-per-rank", type=int, default=0,
@@ -68,12 +86,24 @@ def config_text(name):
         return f.read()
 
 
-def bench_config(n, m, world):
+def workload_of(args, world):
+    return args.workload or ("c5" if world == 1 else "c5s")
+
+
+def bench_config(wl, n, m, world):
     """The workload dict, identical in both arms."""
-    return {"workload": WORKLOAD, "n": n, "m": m, "k": K_NO, "nodes_per_step": C5_NODES,
+    w = WORKLOADS[wl]
+    return {"workload": w["desc"], "name": wl, "n": n, "m": m, "k": w["k"],
+            "nodes_per_step": w["nodes"],
             "l2": "flushed between timed steps (256 MB memset)",
             "parallelism": "1 GPU" if world == 1 else
             f"{world} GPUs, one shard each, worklists linked over NVLink P2P (CUDA IPC)"}
+
+
+def ref_graph(ref, name):
+    """A config graph as the reference parses it (C3/C5/C5-scale solved on the complement)."""
+    g = ref.parse(config_text(name), dimacs=True)
+    return ref.complement(g) if name in ("c3", "c5", "c5s") else g
 
 
 # ---------------------------------------------------------------- clocks during the timed region
@@ -153,13 +183,13 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+def ncu_traffic(key="dense_kernel_c5"):
+    """dram bytes per launch of a kernel from the committed ncu summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dense_kernel_c5", {}).get("dram_bytes_per_launch")
+        return d.get(key, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
@@ -170,51 +200,110 @@ def reference_line(args, rank, world):
     if rank != 0:
         return
     from oracle.oracle import Reference
+    wl = workload_of(args, world)
+    k, full = WORKLOADS[wl]["k"], WORKLOADS[wl]["nodes"]
     ref = Reference()
-    g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
+    g = ref_graph(ref, wl)
     cores = os.cpu_count() or 1
     budget_s = args.ref_sample_s or max(2.0, min(12.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=1.0)
+        ref.solve(g, pvc=True, k=k, strategy="hybrid", workers=cores, timeout_s=1.0)
     rates, nodes = [], 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=budget_s)
+        r = ref.solve(g, pvc=True, k=k, strategy="hybrid", workers=cores, timeout_s=budget_s)
         rates.append(r["nodes"] / (r["wall_ms"] / 1e3))
         nodes += r["nodes"]
     wall = time.perf_counter() - t0
     value = nodes / wall
-    sample = (f"reference run_hybrid ({cores} threads) on C5 PVC k={K_NO}, each step the first "
-              f"{budget_s:.1f} s of the same search (timeout); full tree {C5_NODES} nodes")
+    sample = (f"reference run_hybrid ({cores} threads) on {wl} PVC k={k}, each step the first "
+              f"{budget_s:.1f} s of the same search (timeout); full tree {full} nodes")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
-        "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
-        "config": bench_config(g.n, g.m, world),
-        "time_to_solution_s_est": C5_NODES / value,
+        "data": f"synthetic (frozen p_hat-style graph, data/configs/{wl}.clq.gz)",
+        "config": bench_config(wl, g.n, g.m, world),
+        "time_to_solution_s_est": full / value,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def cpu_baseline(sample_s):
-    """The reference on the box's host cores, bounded sample (rank 0, N=1 only)."""
+def ref_pvc_rate(name, k, sample_s):
+    """The reference's node rate on a bounded sample of a PVC search (rank 0, N=1 only)."""
     try:
         from oracle.oracle import Reference
         ref = Reference()
     except OSError as e:
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {e}"}
-    g = ref.complement(ref.parse(config_text("c5"), dimacs=True))
+    g = ref_graph(ref, name)
     cores = os.cpu_count() or 1
-    r = ref.solve(g, pvc=True, k=K_NO, strategy="hybrid", workers=cores, timeout_s=sample_s)
+    r = ref.solve(g, pvc=True, k=k, strategy="hybrid", workers=cores, timeout_s=sample_s)
     return {"value": r["nodes"] / (r["wall_ms"] / 1e3), "unit": UNIT, "cores": cores,
             "kind": "reference",
-            "sample": (f"reference run_hybrid, {cores} threads, C5 PVC k={K_NO}: "
+            "sample": (f"reference run_hybrid, {cores} threads, {name} PVC k={k}: "
                        f"{r['nodes']} nodes in {r['wall_ms'] / 1e3:.1f} s "
-                       f"(status {r['status']}; full tree {C5_NODES} nodes)")}
+                       f"(status {r['status']})")}
+
+
+def extras(vc, peak, peak_src):
+    """N=1 extra keys: C1 / C3 MVC time-to-solution, C4 node throughput at a 100k budget (its
+    roofline: SURVEY §8d bytes 2·n·(R+M+C)), and C5-scale — each beside the reference."""
+    from paper_2204_10402_b200.configs import load_config
+    try:
+        from oracle.oracle import Reference
+        ref = Reference()
+    except OSError:
+        ref = None
+    cores = os.cpu_count() or 1
+    out = {}
+    for name in ("c1", "c3"):
+        g = load_config(name)
+        vc.solve_mvc(g, strategy="gpu")  # (warm-up: graph upload, kernel load)
+        runs = [vc.solve_mvc(g, strategy="gpu") for _ in range(5)]
+        r = runs[-1]
+        e = {"answer": r["size"], "time_to_solution_ms": statistics.median(x["wall_ms"] for x in runs),
+             "device_ms": statistics.median(x["device_ms"] for x in runs),
+             "nodes": r["nodes_total"], "strategy": "gpu"}
+        if ref is not None:
+            rg = ref_graph(ref, name)
+            rr = [ref.solve(rg, strategy="hybrid", workers=cores) for _ in range(3)]
+            e["reference"] = {"answer": rr[-1]["size"], "cores": cores,
+                              "time_to_solution_ms": statistics.median(x["wall_ms"] for x in rr),
+                              "runs_ms": [round(x["wall_ms"], 2) for x in rr]}
+        out[f"{name}_mvc"] = e
+    g4 = load_config("c4")
+    vc.solve_mvc(g4, strategy="gpu", node_budget=2000)
+    r = vc.solve_mvc(g4, strategy="gpu", node_budget=100_000)
+    dev_s = r["device_ms"] / 1e3
+    alg = 2 * g4.num_vertices * (r["rounds"] + r["maxdeg_passes"] + r["children"])
+    e = {"node_budget": 100_000, "nodes": r["nodes_total"], "device_ms": r["device_ms"],
+         "nodes_per_s": r["nodes_total"] / dev_s, "rounds": r["rounds"],
+         "roofline": {"bound": "hbm", "achieved": alg / dev_s / 1e9, "peak": peak, "unit": "GB/s",
+                      "frac": alg / dev_s / 1e9 / peak, "traffic": ncu_traffic("sparse_kernel_c4"),
+                      "kernel": "sparse_kernel", "algorithmic_bytes_per_launch": alg,
+                      "bytes_per_node_def": "w*n*(R+M+C), w=2 B (u16 degree array), n=100000",
+                      "peak_source": peak_src}}
+    if ref is not None:
+        rg = ref_graph(ref, "c4")
+        rr = ref.solve(rg, strategy="hybrid", workers=cores, timeout_s=15.0)
+        e["reference"] = {"nodes": rr["nodes"], "wall_ms": rr["wall_ms"], "cores": cores,
+                          "nodes_per_s": rr["nodes"] / (rr["wall_ms"] / 1e3),
+                          "note": "15 s sample of run_hybrid MVC (wall includes its greedy)"}
+    out["c4_budget"] = e
+    w = WORKLOADS["c5s"]
+    gs = load_config("c5s")
+    r = vc.solve_pvc(gs, w["k"], strategy="gpu")
+    out["c5_scale"] = {"workload": w["desc"], "n": gs.num_vertices, "m": gs.num_edges, "k": w["k"],
+                       "answer": "no" if not r["feasible"] else "yes", "nodes": r["nodes_total"],
+                       "nodes_expected": w["nodes"], "time_to_solution_s": r["wall_ms"] / 1e3,
+                       "device_s": r["device_ms"] / 1e3,
+                       "nodes_per_s": r["nodes_total"] / (r["device_ms"] / 1e3),
+                       "cpu_baseline": ref_pvc_rate("c5s", w["k"], 10.0)}
+    return out
 
 
 # ---------------------------------------------------------------- our arm
@@ -224,6 +313,8 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_line(args, rank, world)
+    if args.e2e_steps is None:
+        args.e2e_steps = 5 if world == 1 else 2
 
     import torch
     import torch.distributed as dist
@@ -243,7 +334,9 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         xg = dist.new_group(backend="gloo")
     stream = torch.cuda.Stream()  # the library launches on this stream; events bracket it
-    g = load_config("c5")
+    wl = workload_of(args, world)
+    K_NO = WORKLOADS[wl]["k"]
+    g = load_config(wl)
     n, m = g.num_vertices, g.num_edges
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -266,7 +359,7 @@ def main():
     clocks.start()
     for _ in range(args.warmup):
         r = step()
-        assert not r["feasible"], "C5 k=482 must be infeasible"
+        assert not r["feasible"], f"{wl} k={K_NO} must be infeasible"
         with torch.cuda.stream(stream):
             flush.zero_()  # (the first fill pays torch's lazy kernel load: keep it out of the timing)
 
@@ -381,15 +474,17 @@ def main():
         "time_to_solution_s": elapsed_ms / 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "dtype_note": DTYPE_NOTE,
-        "data": "synthetic (frozen p_hat-style graph, data/configs/c5.clq.gz)",
-        "config": bench_config(n, m, world),
+        "data": f"synthetic (frozen p_hat-style graph, data/configs/{wl}.clq.gz)",
+        "config": bench_config(wl, n, m, world),
         "nodes_per_step": nodes_per_step, "strategy": "gpu",
         "clocks": clk,
         "gpu_launches": sum(r["kernel_launches"] for r in results),
     }
     line.update(line_extra)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_sample_s)
+        line["cpu_baseline"] = ref_pvc_rate(wl, K_NO, args.cpu_sample_s)
+    if world == 1 and not args.no_extras:
+        line["configs"] = extras(vc, *measured_peak())
     print(json.dumps(line), flush=True)
 
 

@@ -25,6 +25,10 @@ CONFIGS = {
     "c5": dict(file="c5.clq.gz", complement=True, mode="pvc-no",
                desc="hard PVC no-instance k = MVC-1 on the complement of p_hat-style "
                     "G(500, a=0.25, b=0.75)"),
+    # C5-scale ("pick the C5 density so that 1-GPU time >= ~10 s"): p_hat500-3-like
+    "c5s": dict(file="c5s.clq.gz", complement=True, mode="pvc-no",
+                desc="strong-scaling PVC no-instance k = MVC-1 = 448 on the complement of "
+                     "p_hat-style G(500, a=0.48, b=1.0)"),
 }
 
 

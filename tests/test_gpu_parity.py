@@ -685,3 +685,19 @@ def test_sparse_frontier_expansion_partitions_exactly(oracle):
     f4 = expand_frontier(c4, "mvc", 0, 32)
     assert len(f4["seeds"]) >= 32 or f4["found"]
     assert f4["seeds"].shape[1] == c4.num_vertices + 2
+
+
+def test_c5_scale_no_instance():
+    """C5-scale (the strong-scaling config): PVC(448) visits the cross-checked tree size (see
+    tests/golden/c5s.json) and PVC(449) is a yes with a verified cover."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c5s.json")))
+    g = load_config("c5s")
+    assert g.num_vertices == gold["n"] and g.num_edges == gold["m"]
+    r = vc.solve_pvc(g, gold["pvc_no_k"], strategy="gpu")
+    assert not r["feasible"] and r["status"] == "complete"
+    assert r["nodes_total"] == gold["pvc_no_nodes"]
+    y = vc.solve_pvc(g, gold["pvc_yes_k"], strategy="gpu")
+    assert y["feasible"] and y["size"] <= gold["pvc_yes_k"]
+    check_cover(g, y)

@@ -3,7 +3,7 @@
 for rep in 1 2; do
   echo "== main"; timeout 120 python tools/probe.py c5 2>&1 | grep pvc482 | cut -c1-200
   for v in "$@"; do
-    echo "== $v"; VCGPU_LIB=paper_2204_10402_b200/variants/$v/libvcgpu.so timeout 120 python tools/probe.py c5 2>&1 | grep pvc482 | cut -c1-200
+    echo "== $v"; VCGPU_LIB=variants/$v/libvcgpu.so timeout 120 python tools/probe.py c5 2>&1 | grep pvc482 | cut -c1-200
   done
 done
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv

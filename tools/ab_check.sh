@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B with correctness: for the product lib and each variant, C5/C1 probe + a GPU test subset.
 for v in main "$@"; do
-  if [ "$v" = main ]; then unset VCGPU_LIB; else export VCGPU_LIB=paper_2204_10402_b200/variants/$v/libvcgpu.so; fi
+  if [ "$v" = main ]; then unset VCGPU_LIB; else export VCGPU_LIB=variants/$v/libvcgpu.so; fi
   echo "== $v"
   timeout 120 python tools/probe.py c5 c1 2>&1 | grep -E "pvc482|pvc84" | python3 -c "
 import sys, json

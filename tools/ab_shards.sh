@@ -1,7 +1,7 @@
 #!/bin/bash
 # Multi-shard A/B on one device: 2 and 4 shards of C5 k=482 (root start), product lib vs variants.
 for v in main "$@"; do
-  if [ "$v" = main ]; then unset VCGPU_LIB; else export VCGPU_LIB=paper_2204_10402_b200/variants/$v/libvcgpu.so; fi
+  if [ "$v" = main ]; then unset VCGPU_LIB; else export VCGPU_LIB=variants/$v/libvcgpu.so; fi
   echo "== $v"
   timeout 120 python -c "
 import sys, json; sys.path.insert(0, '.')

@@ -1,10 +1,10 @@
 #!/bin/bash
-# Builds libvcgpu.so with extra -D flags into paper_2204_10402_b200/variants/NAME/ (A/B runs:
-# VCGPU_LIB=paper_2204_10402_b200/variants/NAME/libvcgpu.so python tools/probe.py c5).
+# Builds libvcgpu.so with extra -D flags into variants/NAME/ (A/B runs, outside the package:
+# VCGPU_LIB=variants/NAME/libvcgpu.so python tools/probe.py c5).
 set -e
 cd "$(dirname "$0")/.."
 NAME=$1; shift
-OUT=paper_2204_10402_b200/variants/$NAME
+OUT=variants/$NAME
 mkdir -p $OUT/obj
 SRC=paper_2204_10402_b200/csrc
 for f in $SRC/*.cu; do

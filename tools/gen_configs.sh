@@ -9,4 +9,5 @@ mkdir -p data/configs
 /tmp/gen_configs phat 300 0 0.5 0 data/configs/c3.clq
 /tmp/gen_configs ba 100000 3 0 data/configs/c4.clq
 /tmp/gen_configs phat 500 0.25 0.75 0 data/configs/c5.clq
+/tmp/gen_configs phat 500 0.48 1.0 0 data/configs/c5s.clq
 gzip -9 -f data/configs/*.clq
