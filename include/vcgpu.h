@@ -201,6 +201,12 @@ typedef struct {
     uint64_t certify_nodes;
     double certify_ms;
     uint32_t certify_launches;
+    /* search timeline (dense engine): ms after the first worker started by which 10 / 50 / 90 /
+       100% of the workers had taken their first node (the ramp-up), and had exited (the tail);
+       -1 = that share never got work */
+    double t_first_ms[4];
+    double t_end_ms[4];
+    double idle_share;          /* share of the workers' time spent waiting for worklist nodes */
 } vcg_result;
 
 VCG_API void vcg_params_init(vcg_params* p);

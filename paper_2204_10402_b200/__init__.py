@@ -308,6 +308,9 @@ def _result_dict(r):
         phase_cycles=[int(x) for x in r.phase_cycles], active_cycles=int(r.active_cycles),
         donated_peer=int(r.donated_peer),
         certify_nodes=int(r.certify_nodes), certify_ms=float(r.certify_ms),
+        timeline=dict(first_node_ms=[float(x) for x in r.t_first_ms],
+                      exit_ms=[float(x) for x in r.t_end_ms],
+                      idle_share=float(r.idle_share)),
     )
 
 

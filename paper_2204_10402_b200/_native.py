@@ -59,6 +59,7 @@ class Result(C.Structure):
         ("active_cycles", C.c_uint64), ("donated_peer", C.c_uint64),
         ("certify_nodes", C.c_uint64), ("certify_ms", C.c_double),
         ("certify_launches", C.c_uint32),
+        ("t_first_ms", C.c_double * 4), ("t_end_ms", C.c_double * 4), ("idle_share", C.c_double),
     ]
 
 

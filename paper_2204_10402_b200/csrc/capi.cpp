@@ -326,6 +326,11 @@ struct HostRun {
         out->kernel_launches = r.launches;
         for (int i = 0; i < 10; ++i) out->phase_cycles[i] = r.phase[i];
         out->active_cycles = r.active_cycles;
+        for (int i = 0; i < 4; ++i) {
+            out->t_first_ms[i] = r.t_first_ms[i];
+            out->t_end_ms[i] = r.t_end_ms[i];
+        }
+        out->idle_share = r.idle_share;
         out->donated_peer = r.donated_peer;
         out->wall_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

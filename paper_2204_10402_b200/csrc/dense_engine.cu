@@ -212,13 +212,16 @@ void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint
         }
 }
 
+#ifndef VCG_MULTI_MOOL
+#define VCG_MULTI_MOOL false  // the linked-shard kernel with the mid reduction out of line
+#endif
 // Instantiations: (instrumented | plain) single-shard kernels, plus the plain multi-shard one;
 // W = 16 also with the wider mid layout (MW = 8, single-shard).
 template <int W, bool INSTR, int MW = default_mid(W), bool MOOL = false>
 void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s) {
     if (INSTR && a.world > 1)
         throw std::invalid_argument("instrumented runs are single-shard");
-    auto k = a.world > 1 ? dense_kernel<W, false, true>
+    auto k = a.world > 1 ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
              : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
                                             : dense_kernel<W, INSTR, false, false, MW, MOOL>;
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -229,7 +232,7 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
 template <int W, int MW = default_mid(W), bool MOOL = false>
 int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     int nb = 0;
-    auto k = multi ? dense_kernel<W, false, true>
+    auto k = multi ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
                    : (instr ? dense_kernel<W, true, false, false, MW, MOOL>
                             : dense_kernel<W, false, false, false, MW, MOOL>);
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -279,6 +282,32 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
         out.wl_max_size = std::max<uint64_t>(out.wl_max_size, hs[w].max_queue);
         for (int p = 0; p < 10; ++p) out.phase[p] += hs[w].phase[p];
     }
+    // timeline percentiles (workers that never took a node count as never starting)
+    unsigned long long t0 = ~0ull;
+    for (uint32_t w = 0; w < workers; ++w)
+        if (hs[w].t_begin) t0 = std::min(t0, hs[w].t_begin);
+    if (t0 == ~0ull) return;
+    std::vector<double> tf, te;
+    double idle = 0, span = 0;
+    for (uint32_t w = 0; w < workers; ++w) {
+        if (hs[w].t_end > hs[w].t_begin) {
+            span += (double)(hs[w].t_end - hs[w].t_begin);
+            idle += (double)hs[w].t_idle;
+        }
+        if (hs[w].t_first) tf.push_back((hs[w].t_first - t0) * 1e-6);
+        if (hs[w].t_end) te.push_back((hs[w].t_end - t0) * 1e-6);
+    }
+    auto pct = [](std::vector<double>& v, double* o, size_t total) {
+        std::sort(v.begin(), v.end());
+        const double q[4] = {0.1, 0.5, 0.9, 1.0};
+        for (int i = 0; i < 4; ++i) {
+            const size_t k = (size_t)std::ceil(q[i] * total);
+            o[i] = k == 0 ? 0.0 : (k <= v.size() ? v[k - 1] : -1.0);  // -1: never reached
+        }
+    };
+    pct(tf, out.t_first_ms, workers);
+    pct(te, out.t_end_ms, workers);
+    out.idle_share = span > 0 ? idle / span : 0.0;
 }
 
 }  // namespace

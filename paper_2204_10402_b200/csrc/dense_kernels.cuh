@@ -100,6 +100,10 @@ struct WStats {
     unsigned long long nodes, rounds, maxdeg, children, rm1, rm2, rmh, high_water, donated,
         active, max_queue, dooms, peer;
     unsigned long long phase[10];
+    // timeline (globaltimer ns): kernel start, first node taken, exit — the ramp-up and tail of
+    // the search (dense engine)
+    unsigned long long t_begin, t_first, t_end;
+    unsigned long long t_idle;  // ns waiting for a worklist node
 };
 
 enum Phase { PH_WL_REMOVE, PH_WL_ADD, PH_STACK, PH_DEG1, PH_DEG2, PH_HIGH, PH_MAXDEG,
@@ -282,8 +286,8 @@ constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1, REC_MID = 2;
                            // 8 → 10.1, 16 → 9.4, 32 → 9.0, 64 → 9.4)
 #endif
 constexpr uint32_t kPoll = VCG_POLL_EVERY;
-#ifndef VCG_POLL_EVERY_MULTI
-#define VCG_POLL_EVERY_MULTI 8  // linked shards poll more often: the poll also probes a peer
+#ifndef VCG_TEST_GPU_ACQ
+#define VCG_TEST_GPU_ACQ 0  // A/B only (unsound across GPUs): gpu-scope acquires in the shard kernel
 #endif
 #ifndef VCG_WIDE_SMEM
 #define VCG_WIDE_SMEM 1   // wide degrees in shared memory (fewer registers) instead of registers
@@ -1315,6 +1319,109 @@ __device__ __noinline__ bool donate_to_peer(const PeerRef* pr, Ctl* ctl0, Ctl* o
     return true;
 }
 
+// The exchange helper of a linked shard (warp 0 of the shard kernel; it never searches). The
+// search warps run the single-shard loop against their own device worklist; this warp moves
+// queued nodes from it into the worklists of peer shards that run low — over NVLink P2P /
+// CUDA IPC: reserve a slot in the peer's ring with system-scope atomics, copy the record,
+// publish with a system-scope release (the peer's workers acquire at system scope) — and so
+// keeps the peer-specific code and registers out of the search warps (which then hold the
+// single-shard kernel's 24 warps per SM). A node moves only from a shard with more queued
+// nodes than the peer; the peer's `pending` is raised before this shard's drops (termination:
+// see donate_to_peer).
+__device__ __noinline__ void exchange_helper(Ctl* ctl, const PeerRef* peers, uint32_t world,
+                                             uint32_t rank, uint32_t capacity, uint32_t ring_mask,
+                                             uint32_t threshold, unsigned long long entry_bytes,
+                                             unsigned char* wl, unsigned long long* seq,
+                                             WStats* stats, int lane) {
+    uint32_t* const gactive = &peers[0].ctl->gactive;
+    unsigned long long moved = 0;
+    uint32_t rr = 0, sleep = 64;
+#pragma unroll 1
+    while (true) {
+        // 1. stop: cancel, or every shard idle (no queued node, no active worker anywhere)
+        int act = 0;  // 0 wait, 1 move to `target`, 2 stop
+        uint32_t target = 0;
+        if (lane == 0) {
+            const unsigned long long w = ld_relaxed_sys_u64(&ctl->work);
+            if (*reinterpret_cast<volatile uint32_t*>(&ctl->cancel)) {
+                act = 2;
+            } else if ((w >> 32) == 0 && ld_acquire_sys_u32(gactive) == 0) {
+                act = 2;
+            } else {
+                // 2. the poorest peer below its donation threshold, if this shard is richer
+                const uint32_t mine = (uint32_t)w;
+                uint32_t best = ~0u;
+                for (uint32_t i = 1; i < world; ++i) {
+                    const uint32_t p = (rank + i + rr) % world;
+                    const uint32_t q = (uint32_t)ld_relaxed_sys_u64(&peers[p].ctl->work);
+                    if (q < threshold && q + 1 < mine && q < best) {
+                        best = q;
+                        target = p;
+                    }
+                }
+                ++rr;
+                act = best != ~0u ? 1 : 0;
+            }
+        }
+        act = __shfl_sync(FULL, act, 0);
+        if (act == 2) break;
+        if (act == 0) {
+            __nanosleep(sleep);
+            sleep = min(sleep * 2, 2048u);
+            continue;
+        }
+        sleep = 64;
+        target = __shfl_sync(FULL, target, 0);
+        // 3. take the next local node: a ticket, then its publication (it may be a peer's)
+        unsigned long long pos = 0;
+        int got = 0;
+        if (lane == 0) {
+            pos = atomicAdd(&ctl->head, 1ull);
+#pragma unroll 1
+            for (uint32_t spin = 0;; ++spin) {
+                if (ld_acquire_sys_u64(seq + (pos & ring_mask)) == pos + 1) {
+                    got = 1;
+                    break;
+                }
+                if ((spin & 7) == 7) {
+                    if (*reinterpret_cast<volatile uint32_t*>(&ctl->cancel)) break;
+                    if ((ld_relaxed_sys_u64(&ctl->work) >> 32) == 0 && ld_acquire_sys_u32(gactive) == 0)
+                        break;
+                }
+                __nanosleep(64);
+            }
+        }
+        if (!__shfl_sync(FULL, got, 0)) break;
+        pos = __shfl_sync(FULL, pos, 0);
+        (void)ld_acquire_sys_u64(seq + (pos & ring_mask));  // (every lane acquires it)
+        const unsigned char* src = wl + (pos & ring_mask) * entry_bytes;
+        // 4. into the peer's ring (full — a race with other donors — means it has plenty: retry
+        // until it drains; a cancel ends the search anyway)
+        bool sent = false;
+#pragma unroll 1
+        for (uint32_t back = 64;; back = min(back * 2, 2048u)) {
+            sent = donate_to_peer(peers + target, peers[0].ctl, ctl, capacity, ring_mask, entry_bytes,
+                                  src, lane);
+            if (sent) break;
+            int c = 0;
+            if (lane == 0) c = *reinterpret_cast<volatile uint32_t*>(&ctl->cancel);
+            if (__shfl_sync(FULL, c, 0)) break;
+            __nanosleep(back);
+        }
+        __syncwarp();
+        // 5. release the local slot; this shard's queue and pending each drop by one (the peer's
+        // pending was raised first, so the active-shard count never touches zero in between)
+        if (lane == 0) {
+            st_release_sys_u64(seq + (pos & ring_mask), pos + ring_mask + 1);
+            __threadfence_system();
+            const unsigned long long o = atomicAdd_system(&ctl->work, ~(ONE_PENDING | 1ull) + 1ull);
+            if ((o >> 32) == 1) atomicSub_system(gactive, 1u);
+        }
+        moved += sent;
+    }
+    if (lane == 0) stats->peer = moved;
+}
+
 // record_cover (scheduler.cpp:84-108) once the warp holds a cover: MVC keeps it if it beats the
 // bound (every shard's bound is lowered), PVC keeps the first and ends the search everywhere.
 // Returns true when the search is over (PVC). Cold: out of the node loop's code.
@@ -1363,8 +1470,8 @@ template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid
 #define VCG_MINB8 3   // the same for W <= 8 (C1: 3 → 0.98 ms, 4 → 1.08 ms)
 #endif
 #ifndef VCG_MINB_MULTI
-#define VCG_MINB_MULTI 2  // the multi-shard instantiation (W = 16): 128 registers, no spills
-                          // (2 shards on one B200: 14.1 ms vs 16.0 ms at 3 CTAs/SM with spills)
+#define VCG_MINB_MULTI 3  // the linked-shard instantiation: the single-shard kernel's 24 warps per
+                          // SM (its peer code lives in the exchange helper warp)
 #endif
 // MW: the mid layout's width (0 none, 4: <= 128 alive, 8: <= 256 alive — its 8 KB frames leave
 // room for 2 CTAs per SM; for sparse graphs whose nodes stay wide). MOOL: the mid reduction out
@@ -1398,6 +1505,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         }
     }
     __syncwarp();
+    if constexpr (MULTI) {
+        if (worker == 0) {  // linked shards: warp 0 moves queued nodes to starving peers
+            exchange_helper(a.ctl, a.peers, a.world, a.rank, a.capacity, a.ring_mask, a.threshold,
+                            a.entry_bytes, a.wl, a.seq, a.stats, lane);
+            return;
+        }
+    }
 #define t_start (t0s[0])
 #define c_start ((long long)t0s[1])
     // The current node is WIDE (x: all 32*W vertex slots) until at most 64 vertices are alive,
@@ -1435,7 +1549,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         if (j >= a.stack_bound) j -= a.stack_bound;
         return my_stack + (unsigned long long)j * a.entry_bytes;
     };
-    bool have = false, idle = true;
+    bool have = false, idle = true, first_pop = true;
     unsigned long long subtree = 0;  // StackOnly: current sub-tree id
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
@@ -1443,19 +1557,16 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // (small graphs, W <= 8: short trees whose time is latency — bound and cancel news must
     // travel fast, so they keep polling every 8 nodes)
     constexpr uint32_t kPollK = W <= 8 ? 8u : kPoll;
-    bool probe_now = false;  // linked shards: probe a peer every VCG_POLL_EVERY_MULTI nodes
     uint32_t qsize = 0, polls = kPollK - 1;  // (the first node polls)
     bool poll = false;
     uint2 h = make_uint2(0, 0);  // control line: {best, cancel}
     uint32_t hw = 0;             // worklist size
-    // multi-shard: a peer seen below its donation threshold at the last poll (world = none)
     // (the one-worker strategies — seq, StackOnly — are a separate instantiation: the hybrid
     // kernel carries none of their marker / replay code)
     const bool seq_mode_ = ONEW && a.seq_mode;
     const bool stackonly_ = ONEW && a.stackonly;
     const bool multi = MULTI;  // linked shards (a separate instantiation: the single-shard
                                // kernel carries none of the peer code)
-    uint32_t starve = a.world, hp = a.world, probe = 0, hpv = ~0u;
 
     // process_node (scheduler.cpp:125-144) up to the branch: reduce, prune, record a cover.
     auto reduce_under_B = [&](auto& n) {
@@ -1496,7 +1607,6 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
             qsize = __shfl_sync(FULL, hw, 0);
         }
-        if (probe_now) starve = __shfl_sync(FULL, hp, 0);
         const bool prune = n.doom || prune_at(B, n.cc, n.edges);
         st.dooms += n.doom;
         if (prune) return ACT_POP;
@@ -1546,9 +1656,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
         }
         const bool oldest = a.donate_oldest && sp > 0;
-        // a drained peer shard comes first (at start-up only rank 0 holds any work)
-        const bool urgent = multi && (starve >> 16) && sp > 0 && !seq_mode_;
-        if (!urgent && !seq_mode_ && qsize < a.threshold && (oldest || !dead)) {
+        if (!seq_mode_ && qsize < a.threshold && (oldest || !dead)) {
             unsigned long long seen = 0;
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
@@ -1571,18 +1679,6 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 }
                 ++st.donated;
             }
-        }
-        if (multi && !publish && (starve & 0xFFFFu) < a.world && sp > 0 && !seq_mode_) {
-            // Work donation between shards: a peer below its threshold gets this worker's
-            // oldest stacked node, written straight into its ring slot over NVLink / IPC.
-            if (donate_to_peer(a.peers + (starve & 0xFFFFu), a.peers[0].ctl, a.ctl, a.capacity, a.ring_mask,
-                               a.entry_bytes, slot_at(0), lane)) {
-                base = base + 1 == a.stack_bound ? 0 : base + 1;
-                --sp;
-                ++st.donated;
-                ++st.peer;
-            }
-            starve = a.world;  // (re-armed by the next poll)
         }
         if (build && (!dead || seq_mode_)) {
             if (!child) {
@@ -1650,17 +1746,18 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                 release = a.seq + (pos & a.ring_mask);
                 uint32_t sleep = 32;
                 int outcome = 0;  // 1 got, 2 done
+                const unsigned long long w0 = lane == 0 ? globaltimer() : 0ull;
 #pragma unroll 1
                 for (uint32_t spin = 0;; ++spin) {
                     int o = 0;
                     if (lane == 0) {
-                        if ((multi ? ld_acquire_sys_u64(release) : ld_acquire_u64(release)) == pos + 1) o = 1;
+                        if ((multi && !VCG_TEST_GPU_ACQ ? ld_acquire_sys_u64(release) : ld_acquire_u64(release)) == pos + 1) o = 1;
                         else if ((spin & 7) == 7) {
                             if (ld_volatile_v4(ctl).y) o = 2;
                             else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0 &&
                                      (!multi || ld_acquire_sys_u32(&a.peers[0].ctl->gactive) == 0))
                                 o = 2;  // every shard idle: nothing can create work again
-                            else if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+                            else if (worker == (MULTI ? 1u : 0u) && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
                             else if (a.timeout_ns && globaltimer() - t_start >= a.timeout_ns) {
                                 atomicCAS(&ctl->status, 0, 1);
                                 cancel_all(a);
@@ -1673,12 +1770,13 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                     __nanosleep(sleep);
                     sleep = min(sleep * 2, a.backoff_ns);
                 }
+                if (lane == 0) my_stats->t_idle += globaltimer() - w0;  // (cold: idle path)
                 if (outcome == 2) {
                     if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
                     break;
                 }
                 // every lane acquires the publication
-                (void)(multi ? ld_acquire_sys_u64(release) : ld_acquire_u64(release));
+                (void)(multi && !VCG_TEST_GPU_ACQ ? ld_acquire_sys_u64(release) : ld_acquire_u64(release));
                 src = a.wl + (pos & a.ring_mask) * a.entry_bytes;
                 idle = false;
             }
@@ -1714,6 +1812,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
             have = true;
             if (INSTR) st.phase[release ? PH_WL_REMOVE : PH_STACK] += clock64() - t0;
+            if (first_pop) {
+                first_pop = false;
+                if (lane == 0) my_stats->t_first = globaltimer();
+            }
         }
 
         // Every worker polling the one control line at every node queues thousands of reads on
@@ -1722,25 +1824,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         // stale bound only prunes less; the queue size only steers donation). The read is
         // issued here and consumed after the reduction.
         poll = (++polls & (kPollK - 1)) == 0;
-        probe_now = multi && (polls & (VCG_POLL_EVERY_MULTI - 1)) == 0;
         if (poll && lane == 0) {
             h = ld_volatile_v2(ctl);
             hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
-        }
-        if (probe_now && lane == 0) {
-            {
-                // One peer per poll, round robin: is it below its donation threshold? The read
-                // crosses NVLink, so it is consumed one poll later (it has long arrived): the
-                // verdict on the previous probe's peer now, the next peer's read in flight.
-                if (probe) {
-                    const uint32_t p = (a.rank + 1 + (probe - 1) % (a.world - 1)) % a.world;
-                    // (a drained peer — empty queue — outranks this shard's own worklist)
-                    hp = hpv < a.threshold ? (p | (hpv == 0 ? 0x10000u : 0u)) : a.world;
-                }
-                hpv = (uint32_t)ld_relaxed_sys_u64(
-                    &a.peers[(a.rank + 1 + probe % (a.world - 1)) % a.world].ctl->work);
-                ++probe;
-            }
         }
 
         // visit_and_check_limits (scheduler.cpp:63-74), batched per flush_every visits
@@ -1762,7 +1848,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                     atomicCAS(&ctl->status, 0, stop);
                     cancel_all(a);
                 }
-                if (worker == 0 && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
+                if (worker == (MULTI ? 1u : 0u) && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
                 fold_stats(my_stats, st);
             }
             reset_deltas(st);
@@ -1809,6 +1895,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
         fold_stats(my_stats, st);
         my_stats->high_water = st.high_water;
         my_stats->active = clock64() - c_start;
+        my_stats->t_begin = t0s[0];
+        my_stats->t_end = globaltimer();
         my_stats->max_queue = st.max_queue;
 #pragma unroll
         for (int p = 0; p < 10; ++p) my_stats->phase[p] = INSTR ? st.phase[p] : 0ull;

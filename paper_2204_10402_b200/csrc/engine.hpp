@@ -47,6 +47,10 @@ struct SolveOut {
     uint64_t rm1 = 0, rm2 = 0, rmh = 0, dooms = 0;
     uint64_t phase[10] = {0};
     uint64_t active_cycles = 0;
+    // search timeline (dense engine): ms after the first warp started by which 10 / 50 / 90 /
+    // 100% of the workers had taken their first node, and had exited
+    double t_first_ms[4] = {0, 0, 0, 0}, t_end_ms[4] = {0, 0, 0, 0};
+    double idle_share = 0;  // share of the workers' time spent waiting for worklist nodes
     uint64_t donated_peer = 0;
     double device_ms = 0, h2d_ms = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;

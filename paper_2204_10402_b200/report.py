@@ -61,6 +61,6 @@ def make_report(graph, mode, k, strategy, workers, capacity, threshold_fraction,
                 "d2h_bytes", "rounds", "maxdeg_passes", "children", "removals", "donated", "removals_deg1", "removals_deg2", "removals_high", "doomed",
                 "degree_bytes",
                 "n_padded", "engine", "grid_blocks", "block_threads", "kernel_launches", "cover_from_search",
-                "worker_stack_high_water", "certify_nodes", "certify_ms"):
+                "worker_stack_high_water", "certify_nodes", "certify_ms", "timeline"):
         rep[key] = res[key]
     return rep

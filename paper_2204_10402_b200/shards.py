@@ -131,6 +131,7 @@ def combine(graph, mode, frontier, parts, wall_ms):
                 rank_device_ms=[r["device_ms"] for r in parts],
                 rank_donated=[r["donated"] for r in parts],
                 rank_donated_peer=[r["donated_peer"] for r in parts],
+                rank_idle_share=[r.get("timeline", {}).get("idle_share") for r in parts],
                 worker_nodes=[w for r in parts for w in r["worker_nodes"]],
                 kernel_launches=frontier["kernel_launches"] + sum(r["kernel_launches"] for r in parts),
                 greedy_size=max([frontier["greedy_size"]] + [r.get("greedy_size", 0) for r in parts]),

@@ -12,10 +12,10 @@ import paper_2204_10402_b200 as vc
 from paper_2204_10402_b200.shards import solve_sharded
 g = vc.load_graph('$F', complement_input=True)
 r = vc.solve_pvc(g, $K, strategy='gpu')
-print(json.dumps(dict(shards=1, nodes=r['nodes_total'], ms=round(r['device_ms'], 1))), flush=True)
+print(json.dumps(dict(shards=1, nodes=r['nodes_total'], ms=round(r['device_ms'], 1), idle=r['timeline']['idle_share'])), flush=True)
 for devs in ((0, 0), (0, 0, 0, 0)):
     r = solve_sharded(g, 'pvc', $K, devices=devs)
     print(json.dumps(dict(shards=len(devs), nodes=r['nodes_total'], ms=round(max(r['rank_device_ms']), 1),
-                          rank_nodes=r['rank_nodes'], peer=r['rank_donated_peer'])), flush=True)
+                          rank_nodes=r['rank_nodes'], peer=r['rank_donated_peer'], idle=r['rank_idle_share'])), flush=True)
 "
 done
