@@ -164,6 +164,12 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1) {
 #define VCG_FLUSH_EVERY 64  // visits between a worker's node-counter flushes / limit checks
 #endif
 
+// threads per CTA of the sparse engine's global-memory node variant (4 CTAs per SM)
+#ifndef VCG_GDEG_THREADS
+#define VCG_GDEG_THREADS 256
+#endif
+constexpr uint32_t kGdegThreads = VCG_GDEG_THREADS;
+
 // average degree below which a W = 16 graph runs the <= 256-alive mid layout
 constexpr double kMid8MaxAvgDegree = 24.0;
 // edge density above which a W = 16 graph keeps the mid reduction out of line (see dense_kernel)
@@ -838,11 +844,17 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     }
     const DeviceGraph& dg = *g.dev[dev];
 
+    // CTA size: the shared-memory node takes the SM (1024 threads); the global-memory node
+    // runs smaller CTAs, several per SM (block_warps overrides), so that one node's barrier
+    // waits overlap another's work
+    const uint32_t threads = s.block_warps ? std::min<uint32_t>(s.block_warps, 32) * 32
+                                           : (gdeg ? kGdegThreads : SP_THREADS);
+    const uint32_t per_sm = gdeg ? std::max<uint32_t>(1, std::min<uint32_t>(8, 1024 / threads)) : 1;
     uint32_t workers = s.workers;
     if (s.strategy == 1) workers = 1;
-    if (workers == 0) workers = (uint32_t)C.sms;  // one CTA (a 1024-thread worker) per SM
+    if (workers == 0) workers = (uint32_t)C.sms * per_sm;
     out.grid = workers;
-    out.block = SP_THREADS;
+    out.block = threads;
 
     // stack depth: the reference bound (greedy / min(k, n)), capped by device memory
     size_t free_b = 0, total_b = 0;
@@ -951,7 +963,7 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     auto kern = gdeg ? sparse_kernel<false, true> : sparse_kernel<false, false>;
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaEventRecord(C.ev0, st));
-    kern<<<workers, SP_THREADS, smem, st>>>(a);
+    kern<<<workers, threads, smem, st>>>(a);
     CUDA_CHECK(cudaGetLastError());
     const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
     if (hc.status == 3)

@@ -30,7 +30,8 @@
 
 namespace vcg {
 
-constexpr uint32_t SP_THREADS = 1024;
+constexpr uint32_t SP_THREADS = 1024;  // the largest CTA (shared-memory node: one per SM);
+                                       // the global-memory variant runs 256-thread CTAs, 4 per SM
 constexpr uint16_t DREM = 0xFFFFu;
 
 struct SparseArgs {
@@ -107,7 +108,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, SpShared& s) {
     __syncthreads();
     if ((threadIdx.x & 31) == 0) s.red[threadIdx.x >> 5] = x;
     __syncthreads();
-    uint32_t t = (threadIdx.x < 32) ? s.red[threadIdx.x] : 0u;
+    uint32_t t = (threadIdx.x < (blockDim.x >> 5)) ? s.red[threadIdx.x] : 0u;
     t = __reduce_add_sync(FULL, t);
     __syncthreads();
     if (threadIdx.x == 0) s.red[0] = t;
@@ -128,7 +129,7 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t x, uint32_t& total, Sp
     if (lane == 31) s.red[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-        const uint32_t t = s.red[lane];
+        const uint32_t t = lane < (int)(blockDim.x >> 5) ? s.red[lane] : 0u;
         uint32_t ti = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -177,7 +178,7 @@ struct CtaNode {
         unsigned long long mk = 0;
         const uint32_t n = a->n;
         const uint4* d4 = reinterpret_cast<const uint4*>(deg);
-        for (uint32_t base = 0; base < a->npad; base += 8 * SP_THREADS) {
+        for (uint32_t base = 0; base < a->npad; base += 8 * blockDim.x) {
             const uint32_t v0 = base + 8 * threadIdx.x;
             const uint4 q = v0 < a->npad ? d4[v0 >> 3] : make_uint4(FULL, FULL, FULL, FULL);
             bool any = false;
@@ -229,7 +230,7 @@ struct CtaNode {
     template <class F>
     __device__ void for_each_neighbor(const uint32_t* list, uint32_t count, F f) {
         SpShared& s = *sh;
-        for (uint32_t base = 0; base < count; base += SP_THREADS) {
+        for (uint32_t base = 0; base < count; base += blockDim.x) {
             const uint32_t t = base + threadIdx.x;
             const uint32_t u = t < count ? list[t] : 0u;
             const uint32_t dg = t < count ? a->off[u + 1] - a->off[u] : 0u;
@@ -238,8 +239,8 @@ struct CtaNode {
             cbuf[threadIdx.x] = u;
             cstart[threadIdx.x] = st;
             __syncthreads();
-            const uint32_t items = min(count - base, SP_THREADS);
-            for (uint32_t ib = 0; ib < total; ib += SP_THREADS) {
+            const uint32_t items = min(count - base, (uint32_t)blockDim.x);
+            for (uint32_t ib = 0; ib < total; ib += blockDim.x) {
                 const uint32_t idx = ib + threadIdx.x;
                 const bool valid = idx < total;
                 uint32_t uu = 0, w = 0;
@@ -326,7 +327,7 @@ struct CtaNode {
         SpShared& s = *sh;
         if (threadIdx.x == 0) s.nA = 0;
         __syncthreads();
-        for (uint32_t base = 0; base < count; base += SP_THREADS) {
+        for (uint32_t base = 0; base < count; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             const uint32_t v = i < count ? list[i] : 0u;
             append(i < count && deg[v] == d, v, L, &s.nA);
@@ -359,7 +360,7 @@ struct CtaNode {
         const uint32_t c = s.nA;
         if (threadIdx.x == 0) s.nrem = 0;
         __syncthreads();
-        for (uint32_t base = 0; base < c; base += SP_THREADS) {
+        for (uint32_t base = 0; base < c; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             bool take = false;
             uint32_t u = 0;
@@ -389,7 +390,7 @@ struct CtaNode {
             s.nrem = 0;
         }
         __syncthreads();
-        for (uint32_t base = 0; base < c; base += SP_THREADS) {
+        for (uint32_t base = 0; base < c; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             bool tri = false;
             uint32_t v = 0, p0 = 0, p1 = 0;
@@ -424,7 +425,7 @@ struct CtaNode {
         __syncthreads();
         const uint32_t nT = s.nT;
         // the smallest proposer of overlapping triangles acts: winners are vertex-disjoint
-        for (uint32_t base = 0; base < nT; base += SP_THREADS) {
+        for (uint32_t base = 0; base < nT; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             bool win = false;
             uint32_t v = 0, p0 = 0, p1 = 0;
@@ -456,7 +457,7 @@ struct CtaNode {
             return 0;
         }
         const uint32_t ep = ++epoch;
-        for (uint32_t i = threadIdx.x; i < c; i += SP_THREADS) {
+        for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
             const uint32_t u = L3[i];
             (void)dclaim(deg, u);
             tag[u] = ep;
@@ -537,7 +538,7 @@ struct CtaNode {
         const uint4* src = reinterpret_cast<const uint4*>(rec + 16);
         uint4* dst = reinterpret_cast<uint4*>(deg);
         const uint32_t nvec = a->npad / 8;
-        for (uint32_t i = threadIdx.x; i < nvec; i += SP_THREADS) dst[i] = __ldcg(src + i);
+        for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = __ldcg(src + i);
         if (threadIdx.x == 0) {
             const uint2 h = __ldcg(reinterpret_cast<const uint2*>(rec));
             sh->cc = h.x;
@@ -551,7 +552,7 @@ struct CtaNode {
     __device__ void store_current(unsigned char* rec) const {
         const uint4* s4 = reinterpret_cast<const uint4*>(deg);
         uint4* d4 = reinterpret_cast<uint4*>(rec + 16);
-        for (uint32_t i = threadIdx.x; i < a->npad / 8; i += SP_THREADS) d4[i] = s4[i];
+        for (uint32_t i = threadIdx.x; i < a->npad / 8; i += blockDim.x) d4[i] = s4[i];
         if (threadIdx.x == 0) *reinterpret_cast<uint4*>(rec) = make_uint4(sh->cc, sh->edges, 0u, 0u);
         __syncthreads();
     }
@@ -559,7 +560,7 @@ struct CtaNode {
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
         uint4* d4 = reinterpret_cast<uint4*>(dst);
         const uint32_t nvec = (uint32_t)(a->entry_bytes / 16);
-        for (uint32_t i = threadIdx.x; i < nvec; i += SP_THREADS) d4[i] = __ldcg(s4 + i);
+        for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) d4[i] = __ldcg(s4 + i);
         __syncthreads();
     }
 
@@ -576,7 +577,7 @@ struct CtaNode {
         __syncthreads();
         // X (in RL), tagged with the epoch
         const uint32_t b0 = a->off[v], b1 = a->off[v + 1];
-        for (uint32_t base = b0; base < b1; base += SP_THREADS) {
+        for (uint32_t base = b0; base < b1; base += blockDim.x) {
             const uint32_t e = base + threadIdx.x;
             const uint32_t w = e < b1 ? a->nbr[e] : 0u;
             const bool al = e < b1 && deg[w] != DREM;
@@ -586,12 +587,12 @@ struct CtaNode {
         // bulk copy of the parent's degrees
         uint4* d4 = reinterpret_cast<uint4*>(rec + 16);
         const uint4* s4 = reinterpret_cast<const uint4*>(deg);
-        for (uint32_t i = threadIdx.x; i < a->npad / 8; i += SP_THREADS) d4[i] = s4[i];
+        for (uint32_t i = threadIdx.x; i < a->npad / 8; i += blockDim.x) d4[i] = s4[i];
         __syncthreads();
         const uint32_t nX = s.nX;
         uint16_t* rd = reinterpret_cast<uint16_t*>(rec + 16);
         uint32_t sx = 0;
-        for (uint32_t i = threadIdx.x; i < nX; i += SP_THREADS) {
+        for (uint32_t i = threadIdx.x; i < nX; i += blockDim.x) {
             const uint32_t u = RL[i];
             sx += deg[u];
             rd[u] = DREM;
@@ -615,7 +616,7 @@ struct CtaNode {
         if ((threadIdx.x & 31) == 0 && ex) atomicAdd(&s.eX, ex);
         __syncthreads();
         const uint32_t na = s.nA;
-        for (uint32_t i = threadIdx.x; i < na; i += SP_THREADS) {
+        for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
             const uint32_t w = LA[i];
             rd[w] = (uint16_t)(deg[w] - cnt[w]);
             cnt[w] = 0;
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
             __syncthreads();
             if (sh.red[4]) {
                 uint32_t* slot = a.cover_slots + (unsigned long long)worker * a.cover_words;
-                for (uint32_t w = tid; w < a.cover_words; w += SP_THREADS) {
+                for (uint32_t w = tid; w < a.cover_words; w += blockDim.x) {
                     uint32_t bits = 0;
                     for (int j = 0; j < 32; ++j) {
                         const uint32_t v = 32 * w + j;
@@ -996,7 +997,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_expand_kernel(SparseExpa
         } else if (sh.edges == 0) {
             flag = 1;
             uint32_t* c = e.covers + (unsigned long long)i * (a.cover_words + 1);
-            for (uint32_t w = threadIdx.x; w < a.cover_words; w += SP_THREADS) {
+            for (uint32_t w = threadIdx.x; w < a.cover_words; w += blockDim.x) {
                 uint32_t bits = 0;
                 for (int j = 0; j < 32; ++j) {
                     const uint32_t v = 32 * w + j;

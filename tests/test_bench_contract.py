@@ -38,3 +38,16 @@ def test_reference_arm_other_ranks_exit_silently():
                           "--steps", "1", "--warmup", "0"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_workloads_and_shared_config():
+    """N=1 defaults to C5 (the headline), N>1 to C5-scale; both arms build the config dict with
+    the same function, so the driver sees identical configs."""
+    sys.path.insert(0, ROOT)
+    import bench
+    ns = type("A", (), {"workload": None})()
+    assert bench.workload_of(ns, 1) == "c5" and bench.workload_of(ns, 8) == "c5s"
+    a = bench.bench_config("c5s", 500, 31127, 4)
+    assert a == bench.bench_config("c5s", 500, 31127, 4)
+    assert a["k"] == 448 and a["nodes_per_step"] == 5969685861 and "C5-scale" in a["workload"]
+    assert bench.WORKLOADS["c5"]["nodes"] == 21461369

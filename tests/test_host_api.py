@@ -291,3 +291,41 @@ def test_shard_combine_rules():
     assert r["size"] == 3 and r["cover"] == [0, 1, 2]
     r = combine(None, "mvc", fr, [part(size=4, feasible=True)], 1.0)
     assert r["size"] == 4 and r["cover"] == [0, 1, 2, 3]  # the frontier's (greedy) certificate
+
+
+# ---- worker semantics of the drop-in strategies (bindings.cpp:174-202 defaults) ------------
+
+def test_hybrid_defaults_fill_the_device_and_fold_the_report():
+    """strategy="hybrid" keeps the reference's num_workers for the report (vcg_params.workers)
+    but leaves the device worker count to the engine (device_workers = 0: fill the device) with
+    the tuned donation policy; device_workers fixes a warp count and the reference's policy;
+    "gpu" reports per warp (workers = 0)."""
+    from paper_2204_10402_b200 import _params
+    p, _ = _params("mvc", 0, "hybrid", None, 4096, 0.5, 8, 50, None, None)
+    assert p.workers == 4 and p.device_workers == 0 and p.donate_oldest == 1
+    p, _ = _params("mvc", 0, "hybrid", 4, 4096, 0.5, 8, 50, None, None, device_workers=64)
+    assert p.workers == 4 and p.device_workers == 64 and p.donate_oldest == 0
+    p, _ = _params("mvc", 0, "gpu", None, 4096, 0.5, 8, 50, None, None)
+    assert p.workers == 0 and p.device_workers == 0 and p.donate_oldest == 1
+    p, _ = _params("mvc", 0, "gpu", 512, 4096, 0.5, 8, 50, None, None)
+    assert p.workers == 0 and p.device_workers == 512
+    p, _ = _params("pvc", 3, "stackonly", 8, 4096, 0.5, 4, 50, None, None)
+    assert p.workers == 8 and p.device_workers == 0
+    with pytest.raises(ValueError):
+        _params("mvc", 0, "hybrid", 4, 4096, 0.5, 8, 50, None, None, device_workers=0)
+    q = _native.Params()
+    _native.lib.vcg_params_init(q)
+    assert q.donate_oldest == 1 and q.device_workers == 0 and q.capacity == 4096
+
+
+def test_engine_names_cover_every_variant():
+    from paper_2204_10402_b200 import _ENGINES
+    assert set(_ENGINES) == {"auto", "dense", "sparse", "dense-wide", "dense-nomid",
+                             "dense-mid8", "dense-mid4", "sparse-global"}
+    with pytest.raises(ValueError):
+        vc.solve_mvc(petersen(), engine="nope")
+
+
+def test_c5_scale_config_loads():
+    g = load_config("c5s")
+    assert g.num_vertices == 500 and g.num_edges == 31127
