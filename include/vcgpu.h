@@ -207,6 +207,8 @@ typedef struct {
     double t_first_ms[4];
     double t_end_ms[4];
     double idle_share;          /* share of the workers' time spent waiting for worklist nodes */
+    double t_lastwait_ms[4];    /* ... by which 10/50/90/100% had entered their final wait: the
+                                   search's tail runs from there to t_end_ms */
 } vcg_result;
 
 VCG_API void vcg_params_init(vcg_params* p);

@@ -310,7 +310,8 @@ def _result_dict(r):
         certify_nodes=int(r.certify_nodes), certify_ms=float(r.certify_ms),
         timeline=dict(first_node_ms=[float(x) for x in r.t_first_ms],
                       exit_ms=[float(x) for x in r.t_end_ms],
-                      idle_share=float(r.idle_share)),
+                      idle_share=float(r.idle_share),
+                      final_wait_ms=[float(x) for x in r.t_lastwait_ms]),
     )
 
 

@@ -60,6 +60,7 @@ class Result(C.Structure):
         ("certify_nodes", C.c_uint64), ("certify_ms", C.c_double),
         ("certify_launches", C.c_uint32),
         ("t_first_ms", C.c_double * 4), ("t_end_ms", C.c_double * 4), ("idle_share", C.c_double),
+        ("t_lastwait_ms", C.c_double * 4),
     ]
 
 

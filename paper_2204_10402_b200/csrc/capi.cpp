@@ -329,6 +329,7 @@ struct HostRun {
         for (int i = 0; i < 4; ++i) {
             out->t_first_ms[i] = r.t_first_ms[i];
             out->t_end_ms[i] = r.t_end_ms[i];
+            out->t_lastwait_ms[i] = r.t_lastwait_ms[i];
         }
         out->idle_share = r.idle_share;
         out->donated_peer = r.donated_peer;

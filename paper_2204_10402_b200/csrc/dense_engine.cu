@@ -293,7 +293,7 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
     for (uint32_t w = 0; w < workers; ++w)
         if (hs[w].t_begin) t0 = std::min(t0, hs[w].t_begin);
     if (t0 == ~0ull) return;
-    std::vector<double> tf, te;
+    std::vector<double> tf, te, tw;
     double idle = 0, span = 0;
     for (uint32_t w = 0; w < workers; ++w) {
         if (hs[w].t_end > hs[w].t_begin) {
@@ -302,6 +302,7 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
         }
         if (hs[w].t_first) tf.push_back((hs[w].t_first - t0) * 1e-6);
         if (hs[w].t_end) te.push_back((hs[w].t_end - t0) * 1e-6);
+        if (hs[w].t_lastwait) tw.push_back((hs[w].t_lastwait - t0) * 1e-6);
     }
     auto pct = [](std::vector<double>& v, double* o, size_t total) {
         std::sort(v.begin(), v.end());
@@ -313,6 +314,7 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
     };
     pct(tf, out.t_first_ms, workers);
     pct(te, out.t_end_ms, workers);
+    pct(tw, out.t_lastwait_ms, workers);
     out.idle_share = span > 0 ? idle / span : 0.0;
 }
 

@@ -103,7 +103,8 @@ struct WStats {
     // timeline (globaltimer ns): kernel start, first node taken, exit — the ramp-up and tail of
     // the search (dense engine)
     unsigned long long t_begin, t_first, t_end;
-    unsigned long long t_idle;  // ns waiting for a worklist node
+    unsigned long long t_idle;      // ns waiting for a worklist node
+    unsigned long long t_lastwait;  // start of the last wait (from then on: the tail)
 };
 
 enum Phase { PH_WL_REMOVE, PH_WL_ADD, PH_STACK, PH_DEG1, PH_DEG2, PH_HIGH, PH_MAXDEG,
@@ -441,11 +442,17 @@ struct WarpNode {
     }
     // search_node.cpp:34-46: smallest id among alive vertices of maximum degree
     __device__ __forceinline__ uint32_t argmax() const {
+        uint32_t dmax;
+        return argmax(dmax);
+    }
+    // (and the maximum degree itself)
+    __device__ __forceinline__ uint32_t argmax(uint32_t& dmax) const {
         uint32_t mx = 0;
 #pragma unroll
         for (int i = 0; i < W; ++i)
             mx = max(mx, alive(i) ? ((D(i) << 11) | (2047u - (32u * i + lane))) : 0u);
         mx = __reduce_max_sync(FULL, mx);
+        dmax = mx >> 11;
         return 2047u - (mx & 2047u);
     }
     // A node whose cover reaches the bound is pruned whatever the remaining rules do
@@ -500,8 +507,8 @@ struct WarpNode {
         c.xcnt = __reduce_add_sync(FULL, __popc(c.xl));
     }
     template <bool TEST>
-    __device__ __forceinline__ bool child_pass(Child& c, int B) const {
-        return child_pass<TEST>(c.xl, c.xcnt, B, c.keepm);
+    __device__ __forceinline__ bool child_pass(Child& c, int B, uint32_t dmax) const {
+        return child_pass<TEST>(c.xl, c.xcnt, B, c.keepm, dmax);
     }
     __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
         store_child(c.keepm, c.xcnt, rec);
@@ -514,7 +521,7 @@ struct WarpNode {
     __device__ __forceinline__ void write_child(uint32_t xl, uint32_t xcnt,
                                                 unsigned char* rec) const {
         uint32_t keepm;
-        (void)child_pass<false>(xl, xcnt, 0, keepm);
+        (void)child_pass<false>(xl, xcnt, 0, keepm, 0u);
         store_child(keepm, xcnt, rec);
     }
     // The popcount pass of the remove-N(v) child: for every survivor w, the degree it loses,
@@ -525,8 +532,10 @@ struct WarpNode {
     // bound it would see at best) — and stops as soon as the count passes the limit. Returns
     // true for such a dead child (scratch is then incomplete).
     template <bool TEST>
+    // (dmax: the node's maximum degree — when even it is within the child's limit no survivor
+    // can stay above it, and the pass skips the doom test's headroom bookkeeping)
     __device__ __forceinline__ bool child_pass(uint32_t xl, uint32_t xcnt, int B,
-                                               uint32_t& keep_out) const {
+                                               uint32_t& keep_out, uint32_t dmax) const {
         // X in registers on every lane; xm = this lane's vertices that X removes
         uint32_t X[W];
         uint32_t xm = 0;
@@ -538,15 +547,18 @@ struct WarpNode {
         const uint32_t keepm = alv & ~xm;  // survivors
         keep_out = keepm;
         uint32_t lim = 0;
+        bool test = TEST;
         if (TEST) {
             const uint32_t c2 = cc + xcnt;
             if ((int)c2 > B) return true;
             lim = limit_of(B, c2);
+            test = dmax > lim;
             // headroom d - lim of the survivors above the child's limit (0: not a candidate);
             // such a survivor stays above iff it loses less than its headroom
+            if (test)
 #pragma unroll
-            for (int i = 0; i < W; ++i)
-                scratch(i) = ((keepm >> i) & 1u) ? (uint32_t)max((int)(D(i) - lim), 0) : 0u;
+                for (int i = 0; i < W; ++i)
+                    scratch(i) = ((keepm >> i) & 1u) ? (uint32_t)max((int)(D(i) - lim), 0) : 0u;
         }
         uint32_t above = 0;
         // rolled pass over vertex words
@@ -561,7 +573,7 @@ struct WarpNode {
                          __popc(c.z & X[4 * q + 2]) + __popc(c.w & X[4 * q + 3]);
                 }
             }
-            if (TEST) {
+            if (TEST && test) {
                 above += __reduce_add_sync(FULL, s < scratch(i) ? 1u : 0u);
                 if (above > lim) return true;
             }
@@ -747,26 +759,79 @@ struct WarpNode {
         const unsigned long long tag = next_tag();
         constexpr uint32_t GNPAD = 32 * GW;
         const uint32_t* gw = reinterpret_cast<const uint32_t*>(dense_smem);
-        uint32_t myid[W];
+        if constexpr (W >= 8) {
+            // Sparse graphs (the <= 256-slot frames run only there): each lane compresses the
+            // graph rows of its own slots — for every frame neighbour (a set bit of row(id) ∩ F,
+            // F = the frame's vertex set as a graph bitmap) its slot is the rank of its bit in F.
+            // O(degree) per slot instead of the ballot build's O(frame slots).
+            uint32_t* F = reinterpret_cast<uint32_t*>(dense_smem) + ssb;  // GW words
+            uint32_t* P = F + GW;                                          // prefix ranks
+            if (lane < GW) F[lane] = 0;
+            __syncwarp();
 #pragma unroll
-        for (int i = 0; i < W; ++i) myid[i] = 32 * i + lane < nalive ? graph_id(32 * i + lane) : 0xFFFFu;
-#pragma unroll 1
-        for (uint32_t t = 0; t < nalive; ++t) {
-            const uint32_t idt = graph_id(t);
-            const uint32_t wj = idt >> 5, bit = idt & 31u;
-            uint32_t row[W];
+            for (int i = 0; i < W; ++i)
+                if (32u * i + lane < nalive) {
+                    const uint32_t id = graph_id(32 * i + lane);
+                    atomicOr(&F[id >> 5], 1u << (id & 31));
+                }
+            __syncwarp();
+            const uint32_t pc = lane < GW ? __popc(F[lane]) : 0u;
+            uint32_t incl = pc;
 #pragma unroll
-            for (int i = 0; i < W; ++i) {
-                const bool b = myid[i] != 0xFFFFu &&
-                               ((gw[((wj >> 2) * GNPAD + myid[i]) * 4 + (wj & 3)] >> bit) & 1u);
-                row[i] = __ballot_sync(FULL, b);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += t;
             }
-            if (lane < Q)
+            if (lane < GW) P[lane] = incl - pc;
+            __syncwarp();
+#pragma unroll 1
+            for (int i = 0; i < W; ++i) {
+                const uint32_t s = 32u * i + lane;
+                uint32_t row[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) row[k] = 0;
+                if (s < nalive) {
+                    const uint32_t id = graph_id(s);
+#pragma unroll 1
+                    for (uint32_t j = 0; j < GW; ++j) {
+                        const uint32_t f = F[j];
+                        uint32_t m = gw[((j >> 2) * GNPAD + id) * 4 + (j & 3)] & f;
+                        while (m) {
+                            const uint32_t b = __ffs(m) - 1;
+                            m &= m - 1;
+                            const uint32_t t = P[j] + __popc(f & ((1u << b) - 1u));
+#pragma unroll
+                            for (int k = 0; k < W; ++k) row[k] |= (t >> 5) == (uint32_t)k ? 1u << (t & 31) : 0u;
+                        }
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < Q; ++q)
-                    if (lane == q)
-                        dense_smem[rb + q * NPAD + t] =
-                            make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+                    dense_smem[rb + q * NPAD + s] =
+                        make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+            }
+        } else {
+            uint32_t myid[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) myid[i] = 32 * i + lane < nalive ? graph_id(32 * i + lane) : 0xFFFFu;
+#pragma unroll 1
+            for (uint32_t t = 0; t < nalive; ++t) {
+                const uint32_t idt = graph_id(t);
+                const uint32_t wj = idt >> 5, bit = idt & 31u;
+                uint32_t row[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    const bool b = myid[i] != 0xFFFFu &&
+                                   ((gw[((wj >> 2) * GNPAD + myid[i]) * 4 + (wj & 3)] >> bit) & 1u);
+                    row[i] = __ballot_sync(FULL, b);
+                }
+                if (lane < Q)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q)
+                        if (lane == q)
+                            dense_smem[rb + q * NPAD + t] =
+                                make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+            }
         }
         alv = 0;
 #pragma unroll
@@ -946,12 +1011,13 @@ struct CompactNode {
         return (row(p) >> q) & 1ull;
     }
     __device__ __forceinline__ void mark_nt(uint32_t v) { nt |= 1ull << v; }
-    __device__ __forceinline__ uint32_t argmax() const {  // search_node.cpp:34-46
+    __device__ __forceinline__ uint32_t argmax(uint32_t& dmax) const {  // search_node.cpp:34-46
         uint32_t mx = 0;
 #pragma unroll
         for (int i = 0; i < H; ++i)
             mx = max(mx, alive(i) ? ((d[i] << 11) | (2047u - (32u * i + lane))) : 0u);
         mx = __reduce_max_sync(FULL, mx);
+        dmax = mx >> 11;
         return 2047u - (mx & 2047u);
     }
     __device__ __forceinline__ bool doomed(int B) const { return doom || (int)cc > B; }
@@ -972,7 +1038,7 @@ struct CompactNode {
     // cover exceeds the bound, or more survivors than its limit stay above it — the round-start
     // doom test of reduce_node on the child's state).
     template <bool TEST>
-    __device__ __forceinline__ bool child_pass(Child& c, int B) const {
+    __device__ __forceinline__ bool child_pass(Child& c, int B, uint32_t) const {
 #pragma unroll
         for (int i = 0; i < H; ++i) c.nd[i] = d[i] - __popcll(r[i] & c.X);
         if (!TEST) return false;
@@ -1626,7 +1692,8 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // node goes instead and the child is stacked) — and continue with remove-v.
     auto branch = [&](auto& n) -> int {
         long long tm = INSTR ? clock64() : 0;
-        const uint32_t v = n.argmax();
+        uint32_t dmax;
+        const uint32_t v = n.argmax(dmax);
         ++st.maxdeg;
         if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
         long long tb = INSTR ? clock64() : 0;
@@ -1649,7 +1716,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             // as visited right here (the reference counts it when it pops it). The one-worker
             // strategies keep the reference's visit ORDER — a search that stops early (PVC yes,
             // budget) must not count it — so they stack a 16-byte marker in its place instead.
-            dead = n.template child_pass<true>(c, B);
+            dead = n.template child_pass<true>(c, B, dmax);
             if (!seq_mode_) {
                 st.nodes += dead;
                 st.dooms += dead;
@@ -1770,7 +1837,10 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
                     __nanosleep(sleep);
                     sleep = min(sleep * 2, a.backoff_ns);
                 }
-                if (lane == 0) my_stats->t_idle += globaltimer() - w0;  // (cold: idle path)
+                if (lane == 0) {  // (cold: the idle path)
+                    my_stats->t_idle += globaltimer() - w0;
+                    my_stats->t_lastwait = w0;
+                }
                 if (outcome == 2) {
                     if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
                     break;

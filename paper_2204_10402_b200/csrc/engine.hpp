@@ -50,6 +50,7 @@ struct SolveOut {
     // search timeline (dense engine): ms after the first warp started by which 10 / 50 / 90 /
     // 100% of the workers had taken their first node, and had exited
     double t_first_ms[4] = {0, 0, 0, 0}, t_end_ms[4] = {0, 0, 0, 0};
+    double t_lastwait_ms[4] = {0, 0, 0, 0};  // ... and had entered their final wait (the tail)
     double idle_share = 0;  // share of the workers' time spent waiting for worklist nodes
     uint64_t donated_peer = 0;
     double device_ms = 0, h2d_ms = 0;

@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         o.peer = 0;
         o.active = clock64() - c_start;
         o.max_queue = st.max_queue;
-        o.t_begin = o.t_first = o.t_end = o.t_idle = 0;  // (the timeline is the dense engine's)
+        o.t_begin = o.t_first = o.t_end = o.t_idle = o.t_lastwait = 0;  // (the timeline is the dense engine's)
 #pragma unroll
         for (int p = 0; p < 10; ++p) o.phase[p] = 0;
         a.stats[worker] = o;

@@ -3,11 +3,12 @@ engine, each solved on the GPU and by the oracle (the C restatement of the refer
 to it by tests/test_oracle.py).
 
 Checked per graph:
-* dense engine (n <= 1024): the MVC size (strategy gpu twice, hybrid with 64 warps, StackOnly
-  with 512 warps — no optimality certificate); the PVC(k = MVC - 1) answer and its node count
-  (schedule independent, so it must equal the reference's exactly); the 1-warp seq order's node
-  count; every returned cover verified;
-* sparse engine (forced): the MVC size and a verified cover.
+* dense engine (n <= 1024): the MVC size (strategy gpu twice, hybrid filling the device,
+  hybrid with 64 warps, StackOnly with 512 warps, two linked shards — no optimality
+  certificate); the PVC(k = MVC - 1) answer and its node count (schedule independent, so it
+  must equal the reference's exactly); the 1-warp seq order's node count; every returned cover
+  verified; the mid layouts run wherever nodes keep 65-256 vertices alive;
+* sparse engine (forced, shared- and global-memory node): the MVC size and a verified cover.
 
 Usage: python tools/fuzz_parity.py SECONDS [seed]   -> one JSON line per graph, then a summary
 """
@@ -21,6 +22,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_10402_b200 as vc  # noqa: E402
 from oracle.oracle import CSR, Oracle  # noqa: E402  (the checker)
+from paper_2204_10402_b200.shards import solve_sharded  # noqa: E402
 
 
 def random_graph(rng):
@@ -66,7 +68,8 @@ def main():
         # updates across thousands of warps; plus a small-worker hybrid and StackOnly
         checks = {}
         for tag, kw in (("gpu", dict(strategy="gpu")), ("gpu2", dict(strategy="gpu")),
-                        ("hybrid64", dict(strategy="hybrid", workers=64)),
+                        ("hybrid", dict(strategy="hybrid")),
+                        ("hybrid64", dict(strategy="hybrid", device_workers=64)),
                         ("stackonly", dict(strategy="stackonly", workers=512, depth=10))):
             r = vc.solve_mvc(g, **kw)
             checks[tag] = r["size"] == want["size"] and vc.verify_cover(g, r["cover"]) \
@@ -84,6 +87,14 @@ def main():
             ok &= y["feasible"] and vc.verify_cover(g, y["cover"]) and y["size"] <= want["size"]
         sp = vc.solve_mvc(g, strategy="gpu", engine="sparse")
         ok &= sp["size"] == want["size"] and vc.verify_cover(g, sp["cover"])
+        checks["sparse"] = sp["size"] == want["size"]
+        sg = vc.solve_mvc(g, strategy="gpu", engine="sparse-global")
+        checks["sparse_global"] = sg["size"] == want["size"] and vc.verify_cover(g, sg["cover"])
+        ok &= checks["sparse_global"]
+        if 16 < n <= 1024:  # two linked shards on the device (exchange helper, peer bound)
+            sh = solve_sharded(g, "mvc", devices=(0, 0))
+            checks["sharded"] = sh["size"] == want["size"] and vc.verify_cover(g, sh["cover"])
+            ok &= checks["sharded"]
         rec["ok"] = bool(ok)
         if not ok:
             rec["checks"] = {k: bool(v) for k, v in checks.items()}
