@@ -282,6 +282,11 @@ def extras(vc, peak, peak_src):
     alg = 2 * g4.num_vertices * (r["rounds"] + r["maxdeg_passes"] + r["children"])
     e = {"node_budget": 100_000, "nodes": r["nodes_total"], "device_ms": r["device_ms"],
          "nodes_per_s": r["nodes_total"] / dev_s, "rounds": r["rounds"],
+         "rule_rounds_per_s": r["rounds"] / dev_s,
+         "note": ("budgeted node rates depend on which part of the tree the schedule reaches "
+                  "(per-node cost varies ~20x with depth); rule rounds/s and the roofline "
+                  "bytes compare across configurations"),
+         "workers": len(r["worker_nodes"]), "block_threads": r["block_threads"],
          "roofline": {"bound": "hbm", "achieved": alg / dev_s / 1e9, "peak": peak, "unit": "GB/s",
                       "frac": alg / dev_s / 1e9 / peak, "traffic": ncu_traffic("sparse_kernel_c4"),
                       "kernel": "sparse_kernel", "algorithmic_bytes_per_launch": alg,

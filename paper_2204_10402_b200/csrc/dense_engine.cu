@@ -164,11 +164,14 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1) {
 #define VCG_FLUSH_EVERY 64  // visits between a worker's node-counter flushes / limit checks
 #endif
 
-// threads per CTA of the sparse engine's global-memory node variant (4 CTAs per SM)
-#ifndef VCG_GDEG_THREADS
-#define VCG_GDEG_THREADS 256
+// sparse engine CTA shape: threads per CTA (one search node each), CTAs per SM at most, and
+// the fewest shared-memory-node CTAs per SM worth keeping the node in shared memory (C4,
+// budget 100k: 1024 x 1 3.6 M rule rounds/s, 256 x 4 3.9 M, 128 x 8 9.1 M)
+#ifndef VCG_SPARSE_THREADS
+#define VCG_SPARSE_THREADS 128
 #endif
-constexpr uint32_t kGdegThreads = VCG_GDEG_THREADS;
+constexpr uint32_t kSparseThreads = VCG_SPARSE_THREADS;
+constexpr uint32_t kSparseMaxCtas = 8, kSparseMinCtas = 4;
 
 // average degree below which a W = 16 graph runs the <= 256-alive mid layout
 constexpr double kMid8MaxAvgDegree = 24.0;
@@ -820,10 +823,31 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     const size_t entry = 16 + 2 * (size_t)npad;
     int max_smem = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    // the degree array in shared memory when it fits, else in global memory (GDEG variant)
-    const size_t list_smem = (2 * SP_THREADS + 1) * 4;
-    const bool gdeg = s.engine == 7 || 2 * (size_t)npad + list_smem + sizeof(SpShared) + 1024 > (size_t)max_smem;
-    const size_t smem = (gdeg ? 0 : 2 * (size_t)npad) + list_smem;
+    // CTA shape: small CTAs (kSparseThreads, block_warps overrides), as many per SM as fit, so
+    // that one node's barrier waits overlap other nodes' work. The node's degree array sits in
+    // shared memory when at least kSparseMinCtas such CTAs fit, else in global memory (GDEG
+    // variant, kSparseMaxCtas per SM); engine 7 forces the global one.
+    int sm_smem = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    uint32_t threads = s.block_warps ? std::min<uint32_t>(s.block_warps, 32) * 32 : kSparseThreads;
+    auto ctas_for = [&](uint32_t t, size_t& node_smem) {
+        node_smem = 2 * (size_t)npad + (2 * (size_t)t + 1) * 4;
+        const size_t cost = node_smem + sizeof(SpShared) + 1024;  // (+ the per-CTA reserve)
+        return cost <= (size_t)max_smem ? (uint32_t)std::min<size_t>(kSparseMaxCtas, sm_smem / cost) : 0u;
+    };
+    size_t node_smem = 0;
+    uint32_t smem_ctas = ctas_for(threads, node_smem);
+    const bool fits_one = smem_ctas >= 1;
+    const bool gdeg = s.engine == 7 || !fits_one || (smem_ctas < kSparseMinCtas && s.engine != 2);
+    if (!gdeg && smem_ctas < kSparseMinCtas && !s.block_warps) {
+        threads = SP_THREADS;  // (engine 2 forced on a big node: one 1024-thread CTA per SM)
+        smem_ctas = ctas_for(threads, node_smem);
+    }
+    const size_t list_smem = (2 * (size_t)threads + 1) * 4;
+    const size_t smem = gdeg ? list_smem : node_smem;
+    const uint32_t thread_ctas = std::max<uint32_t>(1, 2048 / threads);
+    const uint32_t per_sm = std::max<uint32_t>(
+        1, std::min<uint32_t>(gdeg ? kSparseMaxCtas : smem_ctas, thread_ctas));
     out.engine = 2;
     out.degree_bytes = 2;
     out.n_padded = npad;
@@ -846,12 +870,6 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     }
     const DeviceGraph& dg = *g.dev[dev];
 
-    // CTA size: the shared-memory node takes the SM (1024 threads); the global-memory node
-    // runs smaller CTAs, several per SM (block_warps overrides), so that one node's barrier
-    // waits overlap another's work
-    const uint32_t threads = s.block_warps ? std::min<uint32_t>(s.block_warps, 32) * 32
-                                           : (gdeg ? kGdegThreads : SP_THREADS);
-    const uint32_t per_sm = gdeg ? std::max<uint32_t>(1, std::min<uint32_t>(8, 1024 / threads)) : 1;
     uint32_t workers = s.workers;
     if (s.strategy == 1) workers = 1;
     if (workers == 0) workers = (uint32_t)C.sms * per_sm;

@@ -287,6 +287,12 @@ constexpr uint32_t REC_WIDE = 0, REC_COMPACT = 1, REC_MID = 2;
                            // 8 → 10.1, 16 → 9.4, 32 → 9.0, 64 → 9.4)
 #endif
 constexpr uint32_t kPoll = VCG_POLL_EVERY;
+#ifndef VCG_CHILD_DMAX
+#define VCG_CHILD_DMAX 0  // skip the child doom test's bookkeeping when max degree <= limit (C5: 10.3 -> 11.3 ms, C2 unchanged: off)
+#endif
+#ifndef VCG_TIMELINE
+#define VCG_TIMELINE 1    // per-warp first-node time (the timeline's ramp-up)
+#endif
 #ifndef VCG_TEST_GPU_ACQ
 #define VCG_TEST_GPU_ACQ 0  // A/B only (unsound across GPUs): gpu-scope acquires in the shard kernel
 #endif
@@ -552,7 +558,7 @@ struct WarpNode {
             const uint32_t c2 = cc + xcnt;
             if ((int)c2 > B) return true;
             lim = limit_of(B, c2);
-            test = dmax > lim;
+            test = !VCG_CHILD_DMAX || dmax > lim;
             // headroom d - lim of the survivors above the child's limit (0: not a candidate);
             // such a survivor stays above iff it loses less than its headroom
             if (test)
@@ -1882,7 +1888,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
             }
             have = true;
             if (INSTR) st.phase[release ? PH_WL_REMOVE : PH_STACK] += clock64() - t0;
-            if (first_pop) {
+            if (VCG_TIMELINE && first_pop) {
                 first_pop = false;
                 if (lane == 0) my_stats->t_first = globaltimer();
             }

@@ -30,8 +30,8 @@
 
 namespace vcg {
 
-constexpr uint32_t SP_THREADS = 1024;  // the largest CTA (shared-memory node: one per SM);
-                                       // the global-memory variant runs 256-thread CTAs, 4 per SM
+constexpr uint32_t SP_THREADS = 1024;  // the largest CTA (the host picks smaller ones, several
+                                       // per SM; see kSparseThreads)
 constexpr uint16_t DREM = 0xFFFFu;
 
 struct SparseArgs {
@@ -150,8 +150,8 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t x, uint32_t& total, Sp
 
 struct CtaNode {
     uint16_t* deg;        // smem, npad entries
-    uint32_t* cbuf;       // smem, SP_THREADS: chunk vertices
-    uint32_t* cstart;     // smem, SP_THREADS + 1: chunk prefix offsets
+    uint32_t* cbuf;       // smem, blockDim.x: chunk vertices
+    uint32_t* cstart;     // smem, blockDim.x + 1: chunk prefix offsets
     SpShared* sh;
     const SparseArgs* a;
     uint32_t *A1, *A2, *N1, *N2;  // candidate lists: this round (A) and the next (N)
@@ -658,7 +658,7 @@ __device__ __forceinline__ void init_cta_node(CtaNode& x, const SparseArgs& a, u
         x.deg = reinterpret_cast<uint16_t*>(smem4);
         x.cbuf = reinterpret_cast<uint32_t*>(x.deg + a.npad);
     }
-    x.cstart = x.cbuf + SP_THREADS;
+    x.cstart = x.cbuf + blockDim.x;
     x.sh = &sh;
     x.a = &a;
     uint32_t* scr = a.scratch + (unsigned long long)worker * 12ull * a.n;
