@@ -171,11 +171,14 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1) {
 #define VCG_SPARSE_THREADS 128
 #endif
 constexpr uint32_t kSparseThreads = VCG_SPARSE_THREADS;
-constexpr uint32_t kSparseMaxCtas = 8, kSparseMinCtas = 4;
+#ifndef VCG_SPARSE_MAX_CTAS
+#define VCG_SPARSE_MAX_CTAS 8
+#endif
+constexpr uint32_t kSparseMaxCtas = VCG_SPARSE_MAX_CTAS, kSparseMinCtas = VCG_SPARSE_MAX_CTAS < 4 ? VCG_SPARSE_MAX_CTAS : 4;
 
 // average degree below which a W = 16 graph runs the <= 256-alive mid layout
 constexpr double kMid8MaxAvgDegree = 24.0;
-// edge density above which a W = 16 graph keeps the mid reduction out of line (see dense_kernel)
+// edge density above which a W = 16 graph runs without the mid layout
 constexpr double kMidOutOfLineDensity = 0.4;
 
 uint32_t pick_w(uint32_t n) {
@@ -381,7 +384,7 @@ struct DenseRun {
     cudaStream_t st = nullptr;
     bool owned;  // own buffers and events (session) instead of the device arenas
     bool mid8 = false;  // W = 16 kernel with the <= 256-alive mid layout
-    bool mool = false;  // W = 16 kernel with the mid reduction out of line (dense graphs)
+    bool mool = false;  // W = 16 kernel without the mid layout (dense graphs)
     std::vector<void*> allocs;
     void* host = nullptr;
     size_t host_bytes = 0;
@@ -470,18 +473,19 @@ struct DenseRun {
         // whose nodes keep a few hundred vertices alive (C2: 160-255); engine 5 forces it.
         mid8 = W == 16 && !owned && s.engine != 3 && s.engine != 4 && s.engine != 6 &&
                (s.engine == 5 || 2.0 * (double)g.m < kMid8MaxAvgDegree * (double)g.n);
-        // dense graphs (C5, C3: nearly every visit compact) keep the mid reduction out of line
-        mool = W == 16 && !owned && !mid8 &&
-               2.0 * (double)g.m > kMidOutOfLineDensity * (double)g.n * (double)(g.n - 1);
+        // dense graphs (C5, C3: nearly every visit compact) run without the mid layout: its code
+        // only costs them instruction cache (C5: 1.3% of visits would be mid)
+        mool = W == 16 && !owned && !mid8 && s.engine != 6 &&
+               (s.engine == 4 || 2.0 * (double)g.m > kMidOutOfLineDensity * (double)g.n * (double)(g.n - 1));
         // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-        smem = dense_smem_bytes(W, block_warps, mid8 ? 8 : -1);
+        smem = dense_smem_bytes(W, block_warps, mid8 ? 8 : (mool ? 0 : -1));
         int per_sm = 1;
         switch (W) {
             case 4: per_sm = occupancy<4>(block, smem, s.instrument, owned); break;
             case 8: per_sm = occupancy<8>(block, smem, s.instrument, owned); break;
             case 16:
                 per_sm = mid8 ? occupancy<16, 8>(block, smem, s.instrument, owned)
-                              : mool ? occupancy<16, 4, true>(block, smem, s.instrument, owned)
+                              : mool ? occupancy<16, 0>(block, smem, s.instrument, owned)
                                      : occupancy<16>(block, smem, s.instrument, owned);
                 break;
             default: per_sm = occupancy<32>(block, smem, s.instrument, owned); break;
@@ -624,7 +628,7 @@ struct DenseRun {
             case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
             case 16:
                 if (mid8) I ? launch_dense<16, true, 8>(a, grid, block, smem, st) : launch_dense<16, false, 8>(a, grid, block, smem, st);
-                else if (mool) I ? launch_dense<16, true, 4, true>(a, grid, block, smem, st) : launch_dense<16, false, 4, true>(a, grid, block, smem, st);
+                else if (mool) I ? launch_dense<16, true, 0>(a, grid, block, smem, st) : launch_dense<16, false, 0>(a, grid, block, smem, st);
                 else I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st);
                 break;
             default: I ? launch_dense<32, true>(a, grid, block, smem, st) : launch_dense<32, false>(a, grid, block, smem, st); break;
@@ -986,6 +990,21 @@ static void solve_sparse(const Graph& g, const SolveSpec& s, SolveOut& out) {
     kern<<<workers, threads, smem, st>>>(a);
     CUDA_CHECK(cudaGetLastError());
     const WStats* hs = finish_and_read(C, st, ctl, stats, workers, hc, out);
+    if (hc.status >= 100) {
+        uint32_t d[12] = {0};
+        CUDA_CHECK(cudaMemcpy(d, cover_slots, sizeof d, cudaMemcpyDeviceToHost));
+        std::string msg = "CUDA error: sparse engine invariant violated at check site " +
+                          std::to_string(hc.status - 100) + " [";
+        for (uint32_t x : d) msg += std::to_string(x) + " ";
+        throw std::runtime_error(msg + "]");
+    }
+    if (hc.status == 4) {
+        uint32_t d[3] = {0, 0, 0};
+        CUDA_CHECK(cudaMemcpy(d, cover_slots, sizeof d, cudaMemcpyDeviceToHost));
+        throw std::runtime_error("CUDA error: sparse engine invariant violated (edges " +
+                                 std::to_string(d[0]) + " with no alive vertex; cc " +
+                                 std::to_string(d[1]) + ", degree sum " + std::to_string(d[2]) + ")");
+    }
     if (hc.status == 3)
         throw std::runtime_error("CUDA error: search stack depth exceeded the device-memory cap (" +
                                  std::to_string(bound) + " nodes per worker) with the worklist full");

@@ -1547,9 +1547,9 @@ template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid
 #endif
 // MW: the mid layout's width (0 none, 4: <= 128 alive, 8: <= 256 alive — its 8 KB frames leave
 // room for 2 CTAs per SM; for sparse graphs whose nodes stay wide). MOOL: the mid reduction out
-// of line — for dense graphs, whose visits are nearly all compact: inlined, the third copy of the
-// rule code costs the compact hot loop registers and instruction cache (C5 9.7 -> 11.9 ms),
-// while out of line the mid node's register degrees go through local memory around the call.
+// of line (an A/B option: out of line, the mid node's register degrees go through local memory
+// around the call; dense graphs, whose visits are nearly all compact, run MW = 0 instead — the
+// mid code inlined costs their compact hot loop registers and instruction cache).
 __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : (MW == 8 ? 2 : VCG_MINB16)) : 1))) dense_kernel(DenseArgs a) {
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;

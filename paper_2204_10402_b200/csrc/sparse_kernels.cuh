@@ -74,6 +74,21 @@ struct SpShared {
     uint32_t red[32];
 };
 
+// Debug builds (VCG_SPARSE_CHECKS=1): vertex ids read from the candidate / removal lists are
+// checked against n; a violation records its site in the status word (100 + site), cancels the
+// search and clamps the id (the host then throws).
+#ifndef VCG_SPARSE_CHECKS
+#define VCG_SPARSE_CHECKS 0
+#endif
+#define SP_CHECK(a, id, site)                                                              \
+    do {                                                                                   \
+        if (VCG_SPARSE_CHECKS && (id) >= (a)->n) {                                         \
+            atomicCAS(&(a)->ctl->status, 0, 100 + (site));                                 \
+            atomicExch(&(a)->ctl->cancel, 1u);                                             \
+            (id) = 0;                                                                      \
+        }                                                                                  \
+    } while (0)
+
 // ---------------------------------------------------------------- block-level helpers
 
 // atomically set deg[v] = 0xFFFF; returns the previous value
@@ -232,7 +247,8 @@ struct CtaNode {
         SpShared& s = *sh;
         for (uint32_t base = 0; base < count; base += blockDim.x) {
             const uint32_t t = base + threadIdx.x;
-            const uint32_t u = t < count ? list[t] : 0u;
+            uint32_t u = t < count ? list[t] : 0u;
+            SP_CHECK(a, u, 1);
             const uint32_t dg = t < count ? a->off[u + 1] - a->off[u] : 0u;
             uint32_t total;
             const uint32_t st = block_exscan(dg, total, s);
@@ -252,6 +268,17 @@ struct CtaNode {
                         else hi = mid - 1;
                     }
                     uu = cbuf[lo];
+                    SP_CHECK(a, uu, 2);
+                    if (VCG_SPARSE_CHECKS && a->off[uu] + (idx - cstart[lo]) >= a->off[uu + 1]) {
+                        if (atomicCAS(&a->ctl->status, 0, 100 + 7) == 0) {
+                            uint32_t* d = a->cover_slots;  // (diagnostics for the host)
+                            d[0] = idx; d[1] = lo; d[2] = items; d[3] = total; d[4] = cstart[lo];
+                            d[5] = a->off[uu + 1] - a->off[uu]; d[6] = count; d[7] = base;
+                            d[8] = threadIdx.x; d[9] = lo + 1 < items ? cstart[lo + 1] : 0xFFFFFFFFu;
+                            d[10] = uu; d[11] = blockDim.x;
+                        }
+                        atomicExch(&a->ctl->cancel, 1u);
+                    }
                     w = a->nbr[a->off[uu] + (idx - cstart[lo])];
                 }
                 f(valid, uu, w);
@@ -313,6 +340,7 @@ struct CtaNode {
 
     // claim u (if still alive) into RL, tagged with the phase epoch
     __device__ __forceinline__ void claim_into_rl(bool want, uint32_t u, uint32_t ep) {
+        if (want) SP_CHECK(a, u, 3);
         const bool got = want && dclaim(deg, u) != DREM;
         if (got) tag[u] = ep;
         append(got, u, RL, &sh->nrem);
@@ -329,8 +357,11 @@ struct CtaNode {
         __syncthreads();
         for (uint32_t base = 0; base < count; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
-            const uint32_t v = i < count ? list[i] : 0u;
-            append(i < count && deg[v] == d, v, L, &s.nA);
+            uint32_t v = i < count ? list[i] : 0u;
+            SP_CHECK(a, v, 4);
+            const bool c = i < count && deg[v] == d;
+            if (c) PP[2 * v] = PP[2 * v + 1] = REM;  // (no partner found yet)
+            append(c, v, L, &s.nA);
         }
         __syncthreads();
         const uint16_t* dg = deg;
@@ -368,7 +399,7 @@ struct CtaNode {
                 const uint32_t v = L[i];
                 u = PP[2 * v];
                 // isolated edge: the smaller id acts (reductions.cpp:7-19 visits it first)
-                take = !(deg[u] == 1 && u < v);
+                take = u != REM && !(deg[u] == 1 && u < v);
             }
             claim_into_rl(take, u, ep);
         }
@@ -400,7 +431,7 @@ struct CtaNode {
                     p0 = PP[2 * v];
                     p1 = PP[2 * v + 1];
                     cnt[v] = 0;  // (counters are zero between uses)
-                    tri = has_edge(p0, p1);
+                    tri = p0 != REM && p1 != REM && p0 != p1 && has_edge(p0, p1);
                     if (tri) {
                         const unsigned long long key = key_hi | v;
                         atomicMin(owner + v, key);
@@ -458,7 +489,8 @@ struct CtaNode {
         }
         const uint32_t ep = ++epoch;
         for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
-            const uint32_t u = L3[i];
+            uint32_t u = L3[i];
+            SP_CHECK(a, u, 5);
             (void)dclaim(deg, u);
             tag[u] = ep;
             RL[i] = u;
@@ -593,7 +625,8 @@ struct CtaNode {
         uint16_t* rd = reinterpret_cast<uint16_t*>(rec + 16);
         uint32_t sx = 0;
         for (uint32_t i = threadIdx.x; i < nX; i += blockDim.x) {
-            const uint32_t u = RL[i];
+            uint32_t u = RL[i];
+            SP_CHECK(a, u, 6);
             sx += deg[u];
             rd[u] = DREM;
         }
@@ -798,17 +831,24 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
 
         // process_node
         x.reduce(best, st);
-        const bool prune = sh.doom || should_prune(a.pvc, a.k, best, sh.cc, sh.edges);
-        st.dooms += sh.doom;
+        // The reduced node's state, read by every thread BEFORE anyone moves on: a thread that
+        // prunes and pops the next record rewrites sh.cc / sh.edges / sh.doom (load_record)
+        // while a slower warp may still be deciding on this node — with small CTAs that skew
+        // split the CTA's control flow and desynchronised its barriers.
+        const uint32_t ncc = sh.cc, nedges = sh.edges;
+        const bool ndoom = sh.doom != 0;
+        __syncthreads();
+        const bool prune = ndoom || should_prune(a.pvc, a.k, best, ncc, nedges);
+        st.dooms += ndoom;
         if (prune) {
             have = false;
             continue;
         }
-        if (sh.edges == 0) {
+        if (nedges == 0) {
             if (tid == 0) {
                 uint32_t rec;
                 if (a.pvc) rec = atomicCAS(&ctl->found, 0u, 1u) == 0u;
-                else rec = sh.cc < atomicMin(&ctl->best, sh.cc);
+                else rec = ncc < atomicMin(&ctl->best, ncc);
                 sh.red[4] = rec;
             }
             __syncthreads();
@@ -825,17 +865,17 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
                 __threadfence();
                 __syncthreads();
                 if (tid == 0) {
-                    atomicMin(&ctl->best_owner, ((unsigned long long)sh.cc << 32) | worker);
+                    atomicMin(&ctl->best_owner, ((unsigned long long)ncc << 32) | worker);
                     if (a.pvc) atomicExch(&ctl->cancel, 1u);
                     if (a.mailbox) {
-                        a.mailbox[2] = sh.cc;
+                        a.mailbox[2] = ncc;
                         if (a.pvc) a.mailbox[3] = 1;
                     }
                 }
             }
             __syncthreads();
             if (a.pvc) break;
-            best = min(best, sh.cc);
+            best = min(best, ncc);
             have = false;
             continue;
         }
@@ -843,6 +883,16 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_kernel(SparseArgs a) {
         x.scan(0xFFFFu, false);
         const uint32_t v = 0xFFFFFFFFu - (uint32_t)(sh.maxkey & 0xFFFFFFFFull);
         ++st.maxdeg;
+        if (v >= a.n) {  // invariant: |E| > 0 implies an alive vertex (fail loudly, status 4)
+            if (tid == 0) {
+                atomicCAS(&ctl->status, 0, 4);
+                atomicExch(&ctl->cancel, 1u);
+                a.cover_slots[0] = sh.edges;
+                a.cover_slots[1] = sh.cc;
+                a.cover_slots[2] = (uint32_t)sh.sumdeg;
+            }
+            break;
+        }
 
         // branch (scheduler.cpp:185-203)
         unsigned char* child = nullptr;

@@ -701,3 +701,19 @@ def test_c5_scale_no_instance():
     y = vc.solve_pvc(g, gold["pvc_yes_k"], strategy="gpu")
     assert y["feasible"] and y["size"] <= gold["pvc_yes_k"]
     check_cover(g, y)
+
+
+def test_sparse_engine_repeated_solves_small_ctas(oracle):
+    """Regression (round 2): with 128-thread CTAs, 8 per SM, a fast thread popping the next node
+    rewrote the shared node state while a slower warp was still deciding on the current one,
+    desynchronising the CTA's barriers (1 solve in ~40 crashed). Many solves of the graph that
+    exposed it, on both node variants."""
+    from oracle.oracle import CSR
+    g = _fuzz_graph("fuzz_gnp_256_549.el")
+    off, nbr = g.csr()
+    want = oracle.solve_seq(CSR(g.num_vertices, g.num_edges, off, nbr))
+    for engine in ("sparse", "sparse-global"):
+        for _ in range(60):
+            r = vc.solve_mvc(g, strategy="gpu", engine=engine)
+            assert r["size"] == want["size"] and r["block_threads"] == 128, (engine, r["size"])
+            check_cover(g, r)
