@@ -242,8 +242,9 @@ VCG_API void vcg_frontier_free(vcg_frontier* f);
 /* Multi-shard solves with device-to-device work donation (SURVEY.md §8e "exchange step").
  * A shard is one dense-engine search (n <= 1024, strategy hybrid) on one GPU with its own device
  * worklist. Linked shards (one per GPU, or several on one device):
- *   - donate their oldest stacked node straight into the ring of a shard whose worklist is
- *     below its threshold (remote stores + a system-scope release over NVLink P2P / CUDA IPC);
+ *   - hand queued nodes straight into the ring of a shard whose worklist is below its
+ *     threshold (an exchange-helper warp per shard: remote stores + a system-scope release
+ *     over NVLink P2P / CUDA IPC);
  *   - propagate an improved MVC bound with peer atomicMin and a PVC "found" / timeout / budget
  *     as a cancel store into every shard;
  *   - terminate together: shard 0 counts the shards whose `pending` (queued + active) is
@@ -258,7 +259,7 @@ VCG_API void vcg_frontier_free(vcg_frontier* f);
  * link_local: link shards opened in this process (same device or P2P-capable devices).
  * launch  : asynchronous; launch EVERY shard before waiting on any (they finish together).
  * wait    : blocks; fills the result like vcg_solve, for this shard's part of the search.
- * On one device, shards must leave room for each other (params.workers), or the later ones
+ * On one device, shards must leave room for each other (params.device_workers), or the later ones
  * cannot become resident. */
 #define VCG_MAX_SHARDS 16
 typedef struct vcg_session vcg_session;
@@ -277,7 +278,8 @@ VCG_API int vcg_session_reset(vcg_session* s);
 VCG_API int vcg_session_wait(vcg_session* s, vcg_result* out);
 VCG_API void vcg_session_close(vcg_session* s);
 /* Workers (warps) of a full-device dense-engine solve of g on `device` (shards sharing a device
- * split them through params.workers). */
+   * split them through params.device_workers). Warp 0 of every linked shard is its exchange
+ * helper (it moves queued nodes to starving peers; the other warps search). */
 VCG_API int vcg_device_workers(const vcg_graph* g, int32_t device, uint32_t* workers);
 
 /* Pinned, device-mapped host words for vcg_params.mailbox (zeroed); n_words >= 4. */

@@ -149,13 +149,23 @@ __global__ void gather_records_kernel(const unsigned char* src, const uint32_t* 
 // Dynamic shared memory of the dense kernels (dense_scratch_base / dense_degree_base): the
 // adjacency bitmap, a W-word slot per warp, W x 32 scratch words per warp, and with
 // VCG_WIDE_SMEM the wide degrees (W x 32 words per warp, laid out after 8 warps of scratch).
-size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1) {
+size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1, uint32_t BW = 8) {
     if (MW < 0) MW = default_mid((int)W);
     const size_t npad = 32 * (size_t)W;
-    const size_t base = W * npad * 4 + 8 * (size_t)W * 4;
-    return VCG_WIDE_SMEM ? base + 8 * (size_t)W * 32 * 4 + warps * (size_t)dense_degree_words(W, MW) * 4
+    const size_t base = W * npad * 4 + BW * (size_t)W * 4;
+    return VCG_WIDE_SMEM ? base + BW * (size_t)W * 32 * 4 + warps * (size_t)dense_degree_words(W, MW) * 4
                          : base + warps * (size_t)W * 32 * 4;
 }
+
+// One large CTA per SM for the W = 16 search kernels (the graph bitmap stored once per SM frees
+// shared memory and the register file for more warps): warps per CTA for the dense-graph
+// kernel (no mid layout) and the 256-slot mid kernel; 0 = the 8-warp CTAs.
+#ifndef VCG_BIG_CTA_DENSE
+#define VCG_BIG_CTA_DENSE 28
+#endif
+#ifndef VCG_BIG_CTA_MID8
+#define VCG_BIG_CTA_MID8 19
+#endif
 
 #ifndef VCG_BACKOFF_CAP_NS
 #define VCG_BACKOFF_CAP_NS 2000  // idle workers' exponential back-off cap
@@ -229,24 +239,29 @@ void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint
 #endif
 // Instantiations: (instrumented | plain) single-shard kernels, plus the plain multi-shard one;
 // W = 16 also with the wider mid layout (MW = 8, single-shard).
-template <int W, bool INSTR, int MW = default_mid(W), bool MOOL = false>
+template <int W, bool INSTR, int MW = default_mid(W), bool MOOL = false, int BW = 8>
 void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s) {
     if (INSTR && a.world > 1)
         throw std::invalid_argument("instrumented runs are single-shard");
-    auto k = a.world > 1 ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
-             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
-                                            : dense_kernel<W, INSTR, false, false, MW, MOOL>;
+    void (*k)(DenseArgs);
+    if constexpr (BW != 8) {
+        k = dense_kernel<W, INSTR, false, false, MW, MOOL, BW>;  // (hybrid single-shard only)
+    } else {
+        k = a.world > 1 ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
+            : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
+                                           : dense_kernel<W, INSTR, false, false, MW, MOOL>;
+    }
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, block, smem, s>>>(a);
     CUDA_CHECK(cudaGetLastError());
 }
 
-template <int W, int MW = default_mid(W), bool MOOL = false>
+template <int W, int MW = default_mid(W), bool MOOL = false, int BW = 8>
 int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     int nb = 0;
     auto k = multi ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
-                   : (instr ? dense_kernel<W, true, false, false, MW, MOOL>
-                            : dense_kernel<W, false, false, false, MW, MOOL>);
+                   : (instr ? dense_kernel<W, true, false, false, MW, MOOL, BW>
+                            : dense_kernel<W, false, false, false, MW, MOOL, BW>);
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)block, smem));
     return nb;
@@ -385,6 +400,7 @@ struct DenseRun {
     bool owned;  // own buffers and events (session) instead of the device arenas
     bool mid8 = false;  // W = 16 kernel with the <= 256-alive mid layout
     bool mool = false;  // W = 16 kernel without the mid layout (dense graphs)
+    bool big = false;   // one large CTA per SM (VCG_BIG_CTA_*)
     std::vector<void*> allocs;
     void* host = nullptr;
     size_t host_bytes = 0;
@@ -467,26 +483,32 @@ struct DenseRun {
         const DeviceGraph& dg = *dgp;
 
         // worker grid: one warp per worker
-        block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : 8;
-        block = 32 * block_warps;
-        // The wider mid layout (<= 256 alive, 8 KB frames, 2 CTAs per SM) for sparse graphs,
-        // whose nodes keep a few hundred vertices alive (C2: 160-255); engine 5 forces it.
+        // The wider mid layout (<= 256 alive, 8 KB frames) for sparse graphs, whose nodes keep a
+        // few hundred vertices alive (C2: 160-255); engine 5 forces it.
         mid8 = W == 16 && !owned && s.engine != 3 && s.engine != 4 && s.engine != 6 &&
                (s.engine == 5 || 2.0 * (double)g.m < kMid8MaxAvgDegree * (double)g.n);
         // dense graphs (C5, C3: nearly every visit compact) run without the mid layout: its code
         // only costs them instruction cache (C5: 1.3% of visits would be mid)
         mool = W == 16 && !owned && !mid8 && s.engine != 6 &&
                (s.engine == 4 || 2.0 * (double)g.m > kMidOutOfLineDensity * (double)g.n * (double)(g.n - 1));
-        // bitmap + per-warp branch mask (W words) + per-warp partial degrees (W x 32 words)
-        smem = dense_smem_bytes(W, block_warps, mid8 ? 8 : (mool ? 0 : -1));
+        // one large CTA per SM for the hybrid single-shard kernels of those two classes
+        big = (mid8 || mool) && !s.block_warps && s.strategy == 0 &&
+              (mid8 ? VCG_BIG_CTA_MID8 : VCG_BIG_CTA_DENSE) > 0;
+        const uint32_t cta_warps = big ? (mid8 ? VCG_BIG_CTA_MID8 : VCG_BIG_CTA_DENSE) : 8;
+        block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : cta_warps;
+        block = 32 * block_warps;
+        // bitmap + per-warp slot (W words) + per-warp scratch and degree / frame words
+        smem = dense_smem_bytes(W, block_warps, mid8 ? 8 : (mool ? 0 : -1), big ? block_warps : 8);
         int per_sm = 1;
         switch (W) {
             case 4: per_sm = occupancy<4>(block, smem, s.instrument, owned); break;
             case 8: per_sm = occupancy<8>(block, smem, s.instrument, owned); break;
             case 16:
-                per_sm = mid8 ? occupancy<16, 8>(block, smem, s.instrument, owned)
-                              : mool ? occupancy<16, 0>(block, smem, s.instrument, owned)
-                                     : occupancy<16>(block, smem, s.instrument, owned);
+                per_sm = big ? (mid8 ? occupancy<16, 8, false, VCG_BIG_CTA_MID8>(block, smem, s.instrument, owned)
+                                     : occupancy<16, 0, false, VCG_BIG_CTA_DENSE>(block, smem, s.instrument, owned))
+                             : mid8 ? occupancy<16, 8>(block, smem, s.instrument, owned)
+                             : mool ? occupancy<16, 0>(block, smem, s.instrument, owned)
+                                    : occupancy<16>(block, smem, s.instrument, owned);
                 break;
             default: per_sm = occupancy<32>(block, smem, s.instrument, owned); break;
         }
@@ -627,7 +649,9 @@ struct DenseRun {
             case 4: I ? launch_dense<4, true>(a, grid, block, smem, st) : launch_dense<4, false>(a, grid, block, smem, st); break;
             case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
             case 16:
-                if (mid8) I ? launch_dense<16, true, 8>(a, grid, block, smem, st) : launch_dense<16, false, 8>(a, grid, block, smem, st);
+                if (big && mid8) I ? launch_dense<16, true, 8, false, VCG_BIG_CTA_MID8>(a, grid, block, smem, st) : launch_dense<16, false, 8, false, VCG_BIG_CTA_MID8>(a, grid, block, smem, st);
+                else if (big) I ? launch_dense<16, true, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st) : launch_dense<16, false, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st);
+                else if (mid8) I ? launch_dense<16, true, 8>(a, grid, block, smem, st) : launch_dense<16, false, 8>(a, grid, block, smem, st);
                 else if (mool) I ? launch_dense<16, true, 0>(a, grid, block, smem, st) : launch_dense<16, false, 0>(a, grid, block, smem, st);
                 else I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st);
                 break;

@@ -307,12 +307,13 @@ constexpr uint32_t kPoll = VCG_POLL_EVERY;
 #endif
 constexpr int kChildUnroll = VCG_CHILD_UNROLL;
 
-// Dynamic shared memory of the dense kernels: the adjacency bitmap ([W/4][32W] uint4 groups),
-// then 8 x W/4 uint4 (reserved), then per warp W x 32 scratch words.
+// Dynamic shared memory of the dense kernels (BW warps per CTA): the adjacency bitmap
+// ([W/4][32W] uint4 groups), then a W-word slot per warp, then per warp W x 32 scratch words,
+// then per warp its degree / frame words.
 extern __shared__ uint4 dense_smem[];
-template <int W>
+template <int W, int BW = 8>
 __device__ __forceinline__ uint32_t dense_scratch_base(uint32_t wib) {
-    return (W / 4) * (32 * W) * 4 + 8 * W + wib * W * 32;
+    return (W / 4) * (32 * W) * 4 + BW * W + wib * W * 32;
 }
 // (VCG_WIDE_SMEM) per-warp degree words after the scratch words of 8 warps; with a mid layout
 // of width MW the region also holds the warp's frame bitmap ([MW/4][32 MW] uint4), which
@@ -323,9 +324,9 @@ __host__ __device__ constexpr uint32_t dense_degree_words(int W, int MW) {
 }
 // the mid width of the default instantiation: 4 (<= 128 alive) where the graph is >= 16 words
 __host__ __device__ constexpr int default_mid(int W) { return W >= 16 ? 4 : 0; }
-template <int W, int MW = default_mid(W)>
+template <int W, int MW = default_mid(W), int BW = 8>
 __device__ __forceinline__ uint32_t dense_degree_base(uint32_t wib) {
-    return dense_scratch_base<W>(8) + wib * dense_degree_words(W, MW);
+    return dense_scratch_base<W, BW>(BW) + wib * dense_degree_words(W, MW);
 }
 
 // WG == 0: the WIDE layout over the whole graph (vertex v at lane v & 31, word v >> 5). WG != 0:
@@ -1534,7 +1535,8 @@ __device__ __noinline__ bool record_cover_(Ctl* ctl, uint32_t* cover_slots, vola
 
 enum { ACT_CONT = 0, ACT_POP = 1, ACT_BREAK = 2, ACT_BRANCH = 3 };
 
-template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid(W), bool MOOL = false>
+template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid(W), bool MOOL = false,
+          int BW = 8>
 #ifndef VCG_MINB16
 #define VCG_MINB16 3  // CTAs of 8 warps per SM targeted by the W=16 register allocation
 #endif               // (wide degrees in smem: 3 → 80 regs, C5 10.2 ms; 2 → 127 regs, 10.8 ms; 4 → 64 + spills, 12.9)
@@ -1550,7 +1552,9 @@ template <int W, bool INSTR, bool MULTI, bool ONEW = false, int MW = default_mid
 // of line (an A/B option: out of line, the mid node's register degrees go through local memory
 // around the call; dense graphs, whose visits are nearly all compact, run MW = 0 instead — the
 // mid code inlined costs their compact hot loop registers and instruction cache).
-__global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : (MW == 8 ? 2 : VCG_MINB16)) : 1))) dense_kernel(DenseArgs a) {
+// BW: warps per CTA — 8 (several CTAs per SM, each with its own copy of the graph bitmap), or one
+// large CTA per SM (the bitmap stored once leaves room for more warps' frames / registers).
+__global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ? VCG_MINB_MULTI : (MW == 8 ? 2 : VCG_MINB16)) : 1)))) dense_kernel(DenseArgs a) {
     constexpr int Q = W / 4;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -1566,6 +1570,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // (the warp's W-word slot between the bitmap and the scratch words; W >= 4)
     unsigned long long* const t0s = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
+    static_assert(BW == 8 || !MULTI, "linked shards use 8-warp CTAs");
     // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
     static_assert(MW == 0 || (W >= 16 && (MW == 4 || MW == 8)), "mid layout width");
     if (lane == 0) {
@@ -1589,9 +1594,9 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     // The current node is WIDE (x: all 32*W vertex slots) until at most 64 vertices are alive,
     // then COMPACT (y: renumbered induced subgraph, see CompactNode).
     WarpNode<W, INSTR> x;
-    x.ssb = dense_scratch_base<W>(wib);
+    x.ssb = dense_scratch_base<W, BW>(wib);
 #if VCG_WIDE_SMEM
-    x.dsb = dense_degree_base<W, MW>(wib);
+    x.dsb = dense_degree_base<W, MW, BW>(wib);
 #endif
     x.lane = lane;
     CompactNode<INSTR> y;
@@ -1601,7 +1606,7 @@ __global__ void __launch_bounds__(256, (W <= 8 ? VCG_MINB8 : (W == 16 ? (MULTI ?
     WarpNode<MW ? MW : 4, INSTR, W> m;
     m.lane = lane;
     m.ssb = x.ssb;
-    m.rb = dense_degree_base<W, MW>(wib) / 4;
+    m.rb = dense_degree_base<W, MW, BW>(wib) / 4;
     m.idb = (x.ssb + (MW ? MW : 4) * 32) * 2;
     m.tgi = (uint32_t)(reinterpret_cast<uint32_t*>(t0s) - reinterpret_cast<uint32_t*>(dense_smem)) / 2 + 2;
     enum { M_WIDE = 0, M_COMPACT = 1, M_MID = 2 };
