@@ -159,12 +159,19 @@ size_t dense_smem_bytes(uint32_t W, uint32_t warps, int MW = -1, uint32_t BW = 8
 
 // One large CTA per SM for the W = 16 search kernels (the graph bitmap stored once per SM frees
 // shared memory and the register file for more warps): warps per CTA for the dense-graph
-// kernel (no mid layout) and the 256-slot mid kernel; 0 = the 8-warp CTAs.
+// kernel (no mid layout), the 256-slot and the 128-slot mid kernels (8 = the 8-warp CTAs,
+// several per SM; 0 = the same for the first two).
 #ifndef VCG_BIG_CTA_DENSE
 #define VCG_BIG_CTA_DENSE 28
 #endif
 #ifndef VCG_BIG_CTA_MID8
 #define VCG_BIG_CTA_MID8 19
+#endif
+#ifndef VCG_BIG_CTA_MID4
+#define VCG_BIG_CTA_MID4 28
+#endif
+#ifndef VCG_BIG_CTA_MULTI
+#define VCG_BIG_CTA_MULTI 28  // the linked-shard kernel (sessions); 8 = 8-warp CTAs
 #endif
 
 #ifndef VCG_BACKOFF_CAP_NS
@@ -245,7 +252,8 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
         throw std::invalid_argument("instrumented runs are single-shard");
     void (*k)(DenseArgs);
     if constexpr (BW != 8) {
-        k = dense_kernel<W, INSTR, false, false, MW, MOOL, BW>;  // (hybrid single-shard only)
+        k = a.world > 1 ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL, BW>
+                        : dense_kernel<W, INSTR, false, false, MW, MOOL, BW>;  // (hybrid only)
     } else {
         k = a.world > 1 ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
@@ -259,7 +267,7 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
 template <int W, int MW = default_mid(W), bool MOOL = false, int BW = 8>
 int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     int nb = 0;
-    auto k = multi ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL>
+    auto k = multi ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL, BW>
                    : (instr ? dense_kernel<W, true, false, false, MW, MOOL, BW>
                             : dense_kernel<W, false, false, false, MW, MOOL, BW>);
     CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -492,9 +500,10 @@ struct DenseRun {
         mool = W == 16 && !owned && !mid8 && s.engine != 6 &&
                (s.engine == 4 || 2.0 * (double)g.m > kMidOutOfLineDensity * (double)g.n * (double)(g.n - 1));
         // one large CTA per SM for the hybrid single-shard kernels of those two classes
-        big = (mid8 || mool) && !s.block_warps && s.strategy == 0 &&
-              (mid8 ? VCG_BIG_CTA_MID8 : VCG_BIG_CTA_DENSE) > 0;
-        const uint32_t cta_warps = big ? (mid8 ? VCG_BIG_CTA_MID8 : VCG_BIG_CTA_DENSE) : 8;
+        const uint32_t big_warps = W != 16 ? 0u : owned ? VCG_BIG_CTA_MULTI
+                                   : mid8 ? VCG_BIG_CTA_MID8 : mool ? VCG_BIG_CTA_DENSE : VCG_BIG_CTA_MID4;
+        big = big_warps > 0 && !s.block_warps && s.strategy == 0;
+        const uint32_t cta_warps = big ? big_warps : 8;
         block_warps = s.block_warps ? std::min<uint32_t>(s.block_warps, 8) : cta_warps;
         block = 32 * block_warps;
         // bitmap + per-warp slot (W words) + per-warp scratch and degree / frame words
@@ -504,8 +513,10 @@ struct DenseRun {
             case 4: per_sm = occupancy<4>(block, smem, s.instrument, owned); break;
             case 8: per_sm = occupancy<8>(block, smem, s.instrument, owned); break;
             case 16:
-                per_sm = big ? (mid8 ? occupancy<16, 8, false, VCG_BIG_CTA_MID8>(block, smem, s.instrument, owned)
-                                     : occupancy<16, 0, false, VCG_BIG_CTA_DENSE>(block, smem, s.instrument, owned))
+                per_sm = big ? (owned ? occupancy<16, 4, false, VCG_BIG_CTA_MULTI>(block, smem, false, true)
+                                : mid8 ? occupancy<16, 8, false, VCG_BIG_CTA_MID8>(block, smem, s.instrument, owned)
+                                : mool ? occupancy<16, 0, false, VCG_BIG_CTA_DENSE>(block, smem, s.instrument, owned)
+                                       : occupancy<16, 4, false, VCG_BIG_CTA_MID4>(block, smem, s.instrument, owned))
                              : mid8 ? occupancy<16, 8>(block, smem, s.instrument, owned)
                              : mool ? occupancy<16, 0>(block, smem, s.instrument, owned)
                                     : occupancy<16>(block, smem, s.instrument, owned);
@@ -650,7 +661,9 @@ struct DenseRun {
             case 8: I ? launch_dense<8, true>(a, grid, block, smem, st) : launch_dense<8, false>(a, grid, block, smem, st); break;
             case 16:
                 if (big && mid8) I ? launch_dense<16, true, 8, false, VCG_BIG_CTA_MID8>(a, grid, block, smem, st) : launch_dense<16, false, 8, false, VCG_BIG_CTA_MID8>(a, grid, block, smem, st);
-                else if (big) I ? launch_dense<16, true, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st) : launch_dense<16, false, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st);
+                else if (big && mool) I ? launch_dense<16, true, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st) : launch_dense<16, false, 0, false, VCG_BIG_CTA_DENSE>(a, grid, block, smem, st);
+                else if (big && owned) launch_dense<16, false, 4, false, VCG_BIG_CTA_MULTI>(a, grid, block, smem, st);
+                else if (big) I ? launch_dense<16, true, 4, false, VCG_BIG_CTA_MID4>(a, grid, block, smem, st) : launch_dense<16, false, 4, false, VCG_BIG_CTA_MID4>(a, grid, block, smem, st);
                 else if (mid8) I ? launch_dense<16, true, 8>(a, grid, block, smem, st) : launch_dense<16, false, 8>(a, grid, block, smem, st);
                 else if (mool) I ? launch_dense<16, true, 0>(a, grid, block, smem, st) : launch_dense<16, false, 0>(a, grid, block, smem, st);
                 else I ? launch_dense<16, true>(a, grid, block, smem, st) : launch_dense<16, false>(a, grid, block, smem, st);
@@ -813,16 +826,18 @@ uint32_t full_device_workers(const Graph& g, int dev) {
     check_dense_device(g, s);
     CUDA_CHECK(cudaSetDevice(dev));
     DeviceCtx& C = ctx_for(dev);
-    const uint32_t W = pick_w(g.n), npad = 32 * W, block = 256;
-    const size_t smem = dense_smem_bytes(W, 8);
+    const uint32_t W = pick_w(g.n);
+    const uint32_t bw = W == 16 ? VCG_BIG_CTA_MULTI : 8;  // (as DenseRun sizes a session)
+    const uint32_t block = 32 * bw;
+    const size_t smem = dense_smem_bytes(W, bw, -1, bw);
     int per_sm = 1;
     switch (W) {
         case 4: per_sm = occupancy<4>(block, smem, false, true); break;
         case 8: per_sm = occupancy<8>(block, smem, false, true); break;
-        case 16: per_sm = occupancy<16>(block, smem, false, true); break;
+        case 16: per_sm = occupancy<16, 4, false, VCG_BIG_CTA_MULTI>(block, smem, false, true); break;
         default: per_sm = occupancy<32>(block, smem, false, true); break;
     }
-    return (uint32_t)C.sms * per_sm * 8;
+    return (uint32_t)C.sms * per_sm * bw;
 }
 
 void session_wait(Session* ses, SolveOut& out) {

@@ -1570,7 +1570,6 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
     // (the warp's W-word slot between the bitmap and the scratch words; W >= 4)
     unsigned long long* const t0s = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
-    static_assert(BW == 8 || !MULTI, "linked shards use 8-warp CTAs");
     // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
     static_assert(MW == 0 || (W >= 16 && (MW == 4 || MW == 8)), "mid layout width");
     if (lane == 0) {
