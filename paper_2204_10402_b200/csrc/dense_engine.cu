@@ -322,7 +322,11 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
     for (uint32_t w = 0; w < workers; ++w)
         if (hs[w].t_begin) t0 = std::min(t0, hs[w].t_begin);
     if (t0 == ~0ull) return;
-    std::vector<double> tf, te, tw;
+    // (on the host's critical path between solves: reused buffers and O(n) selections)
+    thread_local std::vector<double> tf, te, tw;
+    tf.clear();
+    te.clear();
+    tw.clear();
     double idle = 0, span = 0;
     for (uint32_t w = 0; w < workers; ++w) {
         if (hs[w].t_end > hs[w].t_begin) {
@@ -334,11 +338,19 @@ void aggregate(const WStats* hs, uint32_t workers, SolveOut& out) {
         if (hs[w].t_lastwait) tw.push_back((hs[w].t_lastwait - t0) * 1e-6);
     }
     auto pct = [](std::vector<double>& v, double* o, size_t total) {
-        std::sort(v.begin(), v.end());
         const double q[4] = {0.1, 0.5, 0.9, 1.0};
+        size_t lo = 0;  // quantiles ascending: each selection works on the part above the last
         for (int i = 0; i < 4; ++i) {
             const size_t k = (size_t)std::ceil(q[i] * total);
-            o[i] = k == 0 ? 0.0 : (k <= v.size() ? v[k - 1] : -1.0);  // -1: never reached
+            if (k == 0) {
+                o[i] = 0.0;
+            } else if (k > v.size()) {
+                o[i] = -1.0;  // never reached
+            } else {
+                std::nth_element(v.begin() + lo, v.begin() + (k - 1), v.end());
+                o[i] = v[k - 1];
+                lo = k - 1;
+            }
         }
     };
     pct(tf, out.t_first_ms, workers);

@@ -16,9 +16,10 @@ def collect_metrics(worker_nodes, phase_cycles, active_cycles):
     """Load ratios = count / mean (1.0 everywhere if the mean is 0); phase shares = share of the
     workers' active cycles per phase, plus "other" (metrics.cpp:23-67). The device sums cycles
     over workers, so the share is the cycle-weighted mean of per-worker shares."""
-    total = sum(worker_nodes)
-    mean = total / len(worker_nodes) if worker_nodes else 0.0
-    ratios = [w / mean for w in worker_nodes] if mean > 0 else [1.0] * len(worker_nodes)
+    import numpy as np
+    wn = np.asarray(worker_nodes, dtype=np.float64)  # (thousands of device workers)
+    mean = float(wn.mean()) if len(wn) else 0.0
+    ratios = (wn / mean).tolist() if mean > 0 else [1.0] * len(wn)
     shares = {}
     if active_cycles > 0:
         tracked = 0.0
