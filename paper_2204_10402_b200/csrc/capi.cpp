@@ -208,18 +208,23 @@ struct HostRun {
     std::future<vcg::Greedy> greedy_async;
     vcg::SolveSpec s;
 
-    HostRun(const vcg::Graph& g_, const vcg_params* p_, vcg_result* out_)
+    bool greedy_deferred = false;  // PVC: computed by the caller while the search runs
+    vcg::Greedy run_greedy() {
+        const auto a = std::chrono::steady_clock::now();
+        vcg::Greedy gr = vcg::greedy_approx(g);
+        out->greedy_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+        return gr;
+    }
+    // defer_pvc_greedy: the caller runs the PVC greedy itself while the kernel searches
+    // (vcg_solve: solve_on_device's while_running hook) instead of on a new host thread
+    HostRun(const vcg::Graph& g_, const vcg_params* p_, vcg_result* out_, bool defer_pvc_greedy = false)
         : g(g_), p(p_), out(out_), pvc(p_->mode == VCG_PVC), t0(std::chrono::steady_clock::now()) {
         std::memset(out, 0, sizeof(*out));
-        auto run_greedy = [this]() {
-            const auto a = std::chrono::steady_clock::now();
-            vcg::Greedy gr = vcg::greedy_approx(g);
-            out->greedy_ms =
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
-            return gr;
-        };
-        if (pvc && g.n > 0)
-            greedy_async = std::async(std::launch::async, run_greedy);
+        if (pvc && g.n > 0 && defer_pvc_greedy)
+            greedy_deferred = true;
+        else if (pvc && g.n > 0)
+            greedy_async = std::async(std::launch::async, [this]() { return run_greedy(); });
         else
             greedy = run_greedy();
         s.pvc = pvc;
@@ -425,7 +430,7 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
         if (!gh || !p || !out) return fail(VCG_EINVAL, "null argument");
         std::memset(out, 0, sizeof(*out));
         if (const int e = validate(p)) return e;
-        HostRun h(gh->g, p, out);
+        HostRun h(gh->g, p, out, true);
         vcg::SolveOut r;
         if (gh->g.n == 0) {
             // no vertex: one root visit, nothing to branch on (MVC 0; PVC feasible, empty)
@@ -434,7 +439,13 @@ int vcg_solve(const vcg_graph* gh, const vcg_params* p, vcg_result* out) {
             r.found = h.pvc;
             r.wl_added = r.wl_removed = 1;
         } else {
-            vcg::solve_on_device(gh->g, h.s, r);
+            vcg::solve_on_device(gh->g, h.s, r, [&h]() {
+                if (h.greedy_deferred) {
+                    h.greedy = h.run_greedy();
+                    h.greedy_deferred = false;
+                }
+            });
+            if (h.greedy_deferred) h.greedy = h.run_greedy();  // (not reached: the hook ran)
             if (!h.pvc && (p->debug_flags & VCG_DEBUG_CERTIFY) && h.s.strategy != VCG_SEQ)
                 certify_mvc(gh->g, h, r, out);
         }

@@ -34,7 +34,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -104,7 +107,7 @@ struct PinnedArena {
 };
 struct DeviceCtx {
     Arena stacks, wl, seq, misc, scratch, gdeg;
-    PinnedArena host;
+    PinnedArena host, seedbuf;
     cudaStream_t stream = nullptr;
     cudaEvent_t evh = nullptr, ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
@@ -241,6 +244,24 @@ void pack_record(uint32_t W, uint32_t n, uint32_t cc, uint32_t edges, const uint
         }
 }
 
+// Per-process caches of the kernels' shared-memory attribute and occupancy (the CUDA calls cost
+// tens of microseconds on the host path of every solve otherwise).
+std::mutex g_launch_mu;
+std::map<std::tuple<int, const void*, size_t>, bool> g_smem_set;
+std::map<std::tuple<int, const void*, uint32_t, size_t>, int> g_occupancy;
+int current_device() {
+    int d = 0;
+    CUDA_CHECK(cudaGetDevice(&d));
+    return d;
+}
+void set_smem_once(const void* k, size_t smem) {
+    const auto key = std::make_tuple(current_device(), k, smem);
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (g_smem_set.count(key)) return;
+    CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    g_smem_set[key] = true;
+}
+
 #ifndef VCG_MULTI_MOOL
 #define VCG_MULTI_MOOL false  // the linked-shard kernel with the mid reduction out of line
 #endif
@@ -259,7 +280,7 @@ void launch_dense(const DenseArgs& a, uint32_t grid, uint32_t block, size_t smem
             : (a.seq_mode || a.stackonly) ? dense_kernel<W, INSTR, false, true, MW, MOOL>
                                            : dense_kernel<W, INSTR, false, false, MW, MOOL>;
     }
-    CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_once(reinterpret_cast<const void*>(k), smem);
     k<<<grid, block, smem, s>>>(a);
     CUDA_CHECK(cudaGetLastError());
 }
@@ -270,8 +291,16 @@ int occupancy(uint32_t block, size_t smem, bool instr, bool multi = false) {
     auto k = multi ? dense_kernel<W, false, true, false, default_mid(W), VCG_MULTI_MOOL, BW>
                    : (instr ? dense_kernel<W, true, false, false, MW, MOOL, BW>
                             : dense_kernel<W, false, false, false, MW, MOOL, BW>);
-    CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const auto key = std::make_tuple(current_device(), reinterpret_cast<const void*>(k), block, smem);
+    {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        auto it = g_occupancy.find(key);
+        if (it != g_occupancy.end()) return it->second;
+    }
+    set_smem_once(reinterpret_cast<const void*>(k), smem);
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)block, smem));
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    g_occupancy[key] = nb;
     return nb;
 }
 
@@ -424,6 +453,8 @@ struct DenseRun {
     std::vector<void*> allocs;
     void* host = nullptr;
     size_t host_bytes = 0;
+    void* hseed_p = nullptr;
+    size_t hseed_bytes = 0;
     cudaEvent_t evh = nullptr, ev0 = nullptr, ev1 = nullptr;
     std::vector<void*> ipc_opened;
     PeerRef* peers_dev = nullptr;
@@ -447,6 +478,7 @@ struct DenseRun {
         if (peers_dev) cudaFree(peers_dev);
         for (void* p : allocs) cudaFree(p);
         if (host) cudaFreeHost(host);
+        if (hseed_p) cudaFreeHost(hseed_p);
         if (owned) {
             if (evh) cudaEventDestroy(evh);
             if (ev0) cudaEventDestroy(ev0);
@@ -460,6 +492,17 @@ struct DenseRun {
         CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
         allocs.push_back(p);
         return p;
+    }
+    // pinned staging of the initial control block and records (pageable copies would block)
+    void* hseed(size_t bytes) {
+        if (!owned) return C.seedbuf.get(bytes);
+        if (bytes > hseed_bytes) {
+            if (hseed_p) CUDA_CHECK(cudaFreeHost(hseed_p));
+            hseed_p = nullptr;
+            CUDA_CHECK(cudaHostAlloc(&hseed_p, bytes, cudaHostAllocDefault));
+            hseed_bytes = bytes;
+        }
+        return hseed_p;
     }
     void* halloc(size_t bytes) {
         if (!owned) return C.host.get(bytes);
@@ -608,16 +651,20 @@ struct DenseRun {
     // of a persistent multi-shard session (buffers and peer mappings kept).
     void seed() {
         nseeds = s.num_seeds ? s.num_seeds : (s.no_root ? 0 : 1);
-        std::vector<unsigned char> recs(nseeds * entry);
+        // staging: [control block | records], pinned (the stream is idle until the copies land)
+        constexpr size_t kRecsAt = (sizeof(Ctl) + 255) / 256 * 256;
+        unsigned char* stage = static_cast<unsigned char*>(hseed(kRecsAt + nseeds * entry));
+        unsigned char* recs = stage + kRecsAt;
+        const size_t recs_bytes = nseeds * entry;
         if (s.num_seeds) {
             for (uint64_t i = 0; i < nseeds; ++i) {
                 const uint32_t* r = s.seeds + i * (2 + (size_t)g.n);
-                pack_record(W, g.n, r[0], r[1], r + 2, recs.data() + i * entry);
+                pack_record(W, g.n, r[0], r[1], r + 2, recs + i * entry);
             }
         } else if (nseeds) {
             std::vector<uint32_t> deg(g.n);
             for (uint32_t v = 0; v < g.n; ++v) deg[v] = g.degree(v);
-            pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs.data());
+            pack_record(W, g.n, 0, (uint32_t)g.m, deg.data(), recs);
         }
         std::memset(&hc, 0, sizeof(hc));
         hc.best = s.best;
@@ -626,14 +673,15 @@ struct DenseRun {
         hc.work = (nseeds << 32) | nseeds;
         hc.best_owner = ~0ull;
         hc.gactive = active_;  // (read from shard 0's copy only)
-        CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+        std::memcpy(stage, &hc, sizeof(hc));
+        CUDA_CHECK(cudaMemcpyAsync(ctl, stage, sizeof(hc), cudaMemcpyHostToDevice, st));
         if (nseeds)
-            CUDA_CHECK(cudaMemcpyAsync(wl, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+            CUDA_CHECK(cudaMemcpyAsync(wl, recs, recs_bytes, cudaMemcpyHostToDevice, st));
         init_seq_kernel<<<64, 256, 0, st>>>(seq, (uint32_t)ring, (uint32_t)nseeds);
         CUDA_CHECK(cudaGetLastError());
         out.launches += 2;  // init_seq_kernel + dense_kernel
         CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)workers * sizeof(WStats), st));
-        out.h2d_bytes += sizeof(hc) + recs.size();
+        out.h2d_bytes += sizeof(hc) + recs_bytes;
         if (owned) CUDA_CHECK(cudaStreamSynchronize(st));  // (peers may map it before launch)
     }
     uint32_t active_ = 0;  // multi-shard: shards with initial work (shard 0's gactive)
@@ -735,8 +783,12 @@ void check_dense_device(const Graph& g, const SolveSpec& s) {
 }
 }  // namespace
 
-void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
-    if (s.engine == 2 || s.engine == 7 || (s.engine == 0 && g.n > 1024)) return solve_sparse(g, s, out);
+void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out,
+                     const std::function<void()>& while_running) {
+    if (s.engine == 2 || s.engine == 7 || (s.engine == 0 && g.n > 1024)) {
+        if (while_running) while_running();
+        return solve_sparse(g, s, out);
+    }
     check_dense_device(g, s);
     CUDA_CHECK(cudaSetDevice(s.device));
     DeviceCtx& C = ctx_for(s.device);
@@ -745,6 +797,7 @@ void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out) {
     r.out = std::move(out);
     r.prepare();
     r.launch();
+    if (while_running) while_running();  // host work overlapped with the search kernel
     r.finish();
     out = std::move(r.out);
 }

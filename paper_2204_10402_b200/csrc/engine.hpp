@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -75,7 +76,9 @@ struct Frontier {
 void expand_frontier(const Graph& g, const SolveSpec& s, uint64_t target, Frontier& f);
 
 // Throws std::runtime_error (CUDA failures) / std::invalid_argument (bad configuration).
-void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out);
+// while_running: host work to do while the search kernel runs (called after the launch).
+void solve_on_device(const Graph& g, const SolveSpec& s, SolveOut& out,
+                     const std::function<void()>& while_running = {});
 
 // Multi-shard solves (one shard per GPU, or several on one device): each shard is a dense-engine
 // run with its own worklist; linked shards donate work into each other's rings and share the
