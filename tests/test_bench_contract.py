@@ -51,3 +51,16 @@ def test_workloads_and_shared_config():
     assert a == bench.bench_config("c5s", 500, 31127, 4)
     assert a["k"] == 448 and a["nodes_per_step"] == 5969685861 and "C5-scale" in a["workload"]
     assert bench.WORKLOADS["c5"]["nodes"] == 21461369
+
+
+def test_reference_arm_at_n2_times_c5_scale(reference):
+    """Under torchrun (N>1) rank 0 runs the reference on the N>1 workload (C5-scale), with the
+    same config dict as the GPU arm."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-sample-s", "0.5"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["config"]["name"] == "c5s" and d["config"]["k"] == 448 and d["value"] > 0
