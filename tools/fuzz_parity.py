@@ -10,7 +10,8 @@ Checked per graph:
   verified; the mid layouts run wherever nodes keep 65-256 vertices alive;
 * sparse engine (forced, shared- and global-memory node): the MVC size and a verified cover.
 
-Usage: python tools/fuzz_parity.py SECONDS [seed]   -> one JSON line per graph, then a summary
+Usage: python tools/fuzz_parity.py SECONDS [seed] [large]   -> one JSON line per graph, then a
+summary ("large": n > 1024 graphs on the sparse engine)
 """
 import json
 import os
@@ -48,9 +49,55 @@ def random_graph(rng):
     return kind, n, vc.make_graph(n, list(zip(iu[0][keep].tolist(), iu[1][keep].tolist())))
 
 
+def random_large_graph(rng):
+    """n > 1024 (the sparse engine): trees with chords and sparse ER graphs the oracle solves."""
+    n = int(rng.choice([1100, 1500, 2500, 4000, 6000]))
+    if rng.random() < 0.5:
+        edges = [(int(rng.integers(0, v)), v) for v in range(1, n)]
+        edges += [tuple(int(x) for x in rng.integers(0, n, 2)) for _ in range(int(rng.integers(n // 6, n // 2)))]
+        kind = "tree_plus"
+    else:
+        m = int(n * float(rng.uniform(1.0, 1.6)))
+        edges = [tuple(int(x) for x in rng.integers(0, n, 2)) for _ in range(m)]
+        kind = "gnp_sparse"
+    return kind, n, vc.make_graph(n, edges)
+
+
+def main_large(budget, rng):
+    """Large-n randomized parity (sparse engine, shared- and global-memory node): MVC size,
+    PVC(MVC - 1) answer, verified covers."""
+    oracle = Oracle()
+    t0 = time.time()
+    checked = bad = skipped = 0
+    while time.time() - t0 < budget:
+        kind, n, g = random_large_graph(rng)
+        off, nbr = g.csr()
+        csr = CSR(n, g.num_edges, off, nbr)
+        want = oracle.solve_seq(csr, node_budget=60_000)
+        if want["status"] != "complete":
+            skipped += 1
+            continue
+        rec = dict(kind=kind, n=n, m=g.num_edges, mvc=want["size"], seq_nodes=want["nodes"])
+        ok = True
+        for eng in ("auto", "sparse", "sparse-global"):
+            r = vc.solve_mvc(g, strategy="gpu", engine=eng)
+            ok &= r["size"] == want["size"] and r["engine"] == 2 and vc.verify_cover(g, r["cover"])
+            if want["size"] >= 1:
+                p = vc.solve_pvc(g, want["size"] - 1, strategy="gpu", engine=eng)
+                ok &= not p["feasible"]
+        rec["ok"] = bool(ok)
+        checked += 1
+        bad += not ok
+        print(json.dumps(rec), flush=True)
+    print(json.dumps(dict(summary=True, large=True, checked=checked, mismatches=bad, skipped=skipped,
+                          seconds=round(time.time() - t0, 1))), flush=True)
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    if len(sys.argv) > 3 and sys.argv[3] == "large":
+        return main_large(budget, rng)
     oracle = Oracle()
     t0 = time.time()
     checked = bad = skipped = 0
