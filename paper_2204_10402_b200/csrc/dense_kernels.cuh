@@ -312,6 +312,9 @@ constexpr uint32_t kPoll = VCG_POLL_EVERY;
 #ifndef VCG_FROM_WIDE_BALLOT
 #define VCG_FROM_WIDE_BALLOT 1  // compact conversion: rows by ballots over slots (see from_wide)
 #endif
+#ifndef VCG_CNT_SMEM
+#define VCG_CNT_SMEM 1  // (W >= 16) per-branch counters in the warp's shared slot, not registers
+#endif
 #ifndef VCG_CHILD_UNROLL
 #define VCG_CHILD_UNROLL 1  // vertex words per iteration of write_child's popcount loop
 #endif
@@ -1150,17 +1153,27 @@ struct CompactNode {
 #if VCG_FROM_WIDE_BALLOT
         // induced rows, one slot t at a time: lane l tests A[id_l][id_t] and A[id_{l+32}][id_t];
         // by symmetry the two ballots are row t itself (uniform work, no per-bit loops)
+        // Slots are the alive vertices in id order, so walking the alive words and their set
+        // bits in order visits slot t = 0, 1, ...: each lane loads its two rows' word j once
+        // per word (not once per slot) and the slot's column is a register bit test.
         r[0] = r[1] = 0;
+        uint32_t t = 0;
 #pragma unroll 1
-        for (uint32_t t = 0; t < nalive; ++t) {
-            const uint32_t idt = sid[t];
-            const uint32_t wj = idt >> 5, bit = idt & 31u;
-            const bool b0 = id0 != 0xFFFFu && ((w.row_word(id0, wj) >> bit) & 1u);
-            const bool b1 = id1 != 0xFFFFu && ((w.row_word(id1, wj) >> bit) & 1u);
-            const unsigned long long row = ballot2(b0, b1);
-            if (lane == (int)(t & 31u)) {
-                if (t >> 5) r[1] = row;
-                else r[0] = row;
+        for (int j = 0; j < W; ++j) {
+            uint32_t awj = __shfl_sync(FULL, w.aw, j);  // (uniform)
+            if (!awj) continue;
+            const uint32_t w0 = id0 != 0xFFFFu ? w.row_word(id0, j) : 0u;
+            const uint32_t w1 = id1 != 0xFFFFu ? w.row_word(id1, j) : 0u;
+#pragma unroll 1
+            while (awj) {
+                const uint32_t bit = __ffs(awj) - 1;
+                awj &= awj - 1;
+                const unsigned long long row = ballot2((w0 >> bit) & 1u, (w1 >> bit) & 1u);
+                if (lane == (int)(t & 31u)) {
+                    if (t >> 5) r[1] = row;
+                    else r[0] = row;
+                }
+                ++t;
             }
         }
 #else
@@ -1582,9 +1595,19 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
     // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
     static_assert(MW == 0 || (W >= 16 && (MW == 4 || MW == 8)), "mid layout width");
+    // (W >= 16, VCG_CNT_SMEM: words 8..12 hold lane 0's per-branch counters — branches,
+    // children stored, donations, stack high water, queue maximum — instead of five registers
+    // live across the node loop: the hot loop's register budget sets the occupancy, and the
+    // counters change at most once per branch)
+    constexpr bool kCntSmem = VCG_CNT_SMEM && W >= 16;
+    uint32_t* const cw = reinterpret_cast<uint32_t*>(t0s) + 8;
+    enum { CW_MAXDEG = 0, CW_CHILDREN, CW_DONATED, CW_HIGH, CW_MAXQ };
     if (lane == 0) {
         t0s[0] = globaltimer();
         t0s[1] = (unsigned long long)clock64();
+        if (kCntSmem)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) cw[i] = 0;
         if (MW) {
             t0s[2] = 0;  // no frame
             t0s[3] = ((unsigned long long)a.rank << 56) | ((unsigned long long)(worker + 1) << 36);
@@ -1627,6 +1650,12 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
     Counters32 st;
     Ctl* ctl = a.ctl;
 #define my_stats (a.stats + worker)
+    auto fold_cw = [&]() {  // (lane 0)
+        my_stats->maxdeg += cw[CW_MAXDEG];
+        my_stats->children += cw[CW_CHILDREN];
+        my_stats->donated += cw[CW_DONATED];
+        cw[CW_MAXDEG] = cw[CW_CHILDREN] = cw[CW_DONATED] = 0;
+    };
 #define my_stack (a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes)
     // The local stack is a ring [base, base + sp) so its oldest entry can be donated.
     uint32_t base = 0, sp = 0;
@@ -1635,7 +1664,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         if (j >= a.stack_bound) j -= a.stack_bound;
         return my_stack + (unsigned long long)j * a.entry_bytes;
     };
-    bool have = false, idle = true, first_pop = true;
+    bool have = false, idle = true;
     unsigned long long subtree = 0;  // StackOnly: current sub-tree id
     uint32_t replay = 0xFFFFFFFFu;   // StackOnly: levels of the root path replayed so far
     uint32_t best = a.pvc ? a.k : ctl->best;
@@ -1672,28 +1701,26 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         }
     };
     auto settle = [&](auto& n) -> int {
+        // The edge-count prune (should_prune, bounds.cpp:27-29) is a proof only when every
+        // alive degree is within the high-degree limit of the SAME bound (reductions.hpp:25-26):
+        // a cover of L = B - |S| vertices of degree <= L covers at most L^2 edges. The reference
+        // reads one `best` for both (scheduler.cpp:127-132, reductions.cpp:70-87); here the poll
+        // below may lower B after the reduction ran, so the edge test uses Br, the bound the
+        // reduction reached fixpoint under (no cover of size <= Br - |S| proves none <= B - |S|
+        // either), while |S| > B and the doom test prune under the newest bound. (Round 2 first
+        // re-ran the reduction under the lowered bound: a second inlined copy of the compact
+        // reduction in the hot loop, 8% on C5 through instruction-cache misses.)
+        const int Br = B;
         reduce_under_B(n);
         if (VCG_UNLIKELY(poll)) {
             if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
             if (!a.pvc) {
-                // The edge-count prune (should_prune, bounds.cpp:27-29) is a proof only when
-                // every alive degree is within the high-degree limit of the SAME bound
-                // (reductions.hpp:25-26): a cover of L = B - |S| vertices of degree <= L covers
-                // at most L^2 edges. The reduction above ran under the bound seen at the last
-                // poll; if the poll brings a lower one, the node is reduced to fixpoint again
-                // under it before the prune (the reference reads one `best` for both,
-                // scheduler.cpp:127-132, reductions.cpp:70-87). The bound only drops when a
-                // cover improves, so this re-run is rare.
-                const uint32_t nb = __shfl_sync(FULL, h.x, 0);
-                if (nb < best) {
-                    best = nb;
-                    B = bound_of(0, 0, best);
-                    if (!n.doom) reduce_under_B(n);
-                }
+                best = min(best, __shfl_sync(FULL, h.x, 0));
+                B = bound_of(0, 0, best);
             }
             qsize = __shfl_sync(FULL, hw, 0);
         }
-        const bool prune = n.doom || prune_at(B, n.cc, n.edges);
+        const bool prune = n.doom || prune_at(Br, n.cc, n.edges) || (int)n.cc > B;
         st.dooms += n.doom;
         if (prune) return ACT_POP;
         if (VCG_UNLIKELY(n.edges == 0)) {
@@ -1714,7 +1741,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         long long tm = INSTR ? clock64() : 0;
         uint32_t dmax;
         const uint32_t v = n.argmax(dmax);
-        ++st.maxdeg;
+        if (kCntSmem) { if (lane == 0) ++cw[CW_MAXDEG]; } else ++st.maxdeg;
         if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
         long long tb = INSTR ? clock64() : 0;
         // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
@@ -1748,7 +1775,8 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
             int ok = 0;
             if (lane == 0) ok = q_reserve(a, pos, seen);
             if (lane == 0 && ok) {
-                st.max_queue = max(st.max_queue, (uint32_t)seen);
+                if (kCntSmem) cw[CW_MAXQ] = max(cw[CW_MAXQ], (uint32_t)seen);
+                else st.max_queue = max(st.max_queue, (uint32_t)seen);
                 // the slot is free once the previous lap's reader released it
                 if (ld_acquire_u64(a.seq + (pos & a.ring_mask)) != pos)  // (rarely not yet)
                     ok = wait_slot_free(a.seq + (pos & a.ring_mask), pos, &ctl->cancel, false);
@@ -1764,20 +1792,21 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 } else {
                     child = dst;
                 }
-                ++st.donated;
+                if (kCntSmem) { if (lane == 0) ++cw[CW_DONATED]; } else ++st.donated;
             }
         }
         if (build && (!dead || seq_mode_)) {
             if (!child) {
                 child = slot_at(sp);
                 ++sp;
-                if (sp > st.high_water) st.high_water = sp;
+                if (kCntSmem) { if (lane == 0 && sp > cw[CW_HIGH]) cw[CW_HIGH] = sp; }
+                else if (sp > st.high_water) st.high_water = sp;
             }
             if (dead) {
                 if (lane == 0) *reinterpret_cast<uint4*>(child) = make_uint4(DEAD_NODE, 0u, 0u, 0u);
             } else {
                 n.child_store(c, child);
-                ++st.children;
+                if (kCntSmem) { if (lane == 0) ++cw[CW_CHILDREN]; } else ++st.children;
             }
         }
         if (publish) {
@@ -1812,6 +1841,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                     o = (t >> a.depth) == 0 && !ld_volatile_v4(ctl).y;
                 }
                 if (!__shfl_sync(FULL, o, 0)) break;
+                if (VCG_TIMELINE && lane == 0 && !my_stats->t_first) my_stats->t_first = globaltimer();
                 subtree = __shfl_sync(FULL, t, 0);
                 replay = 0;
                 src = a.wl;
@@ -1858,8 +1888,13 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                     sleep = min(sleep * 2, a.backoff_ns);
                 }
                 if (lane == 0) {  // (cold: the idle path)
-                    my_stats->t_idle += globaltimer() - w0;
+                    const unsigned long long now = globaltimer();
+                    my_stats->t_idle += now - w0;
                     my_stats->t_lastwait = w0;
+                    // the first node of a worker always comes off the worklist: its time is
+                    // kept here, off the hot loop (a first-pop flag held in a register across
+                    // the loop cost C5 5% through spills)
+                    if (VCG_TIMELINE && outcome == 1 && !my_stats->t_first) my_stats->t_first = now;
                 }
                 if (outcome == 2) {
                     if (INSTR) st.phase[PH_WL_REMOVE] += clock64() - t0;
@@ -1902,10 +1937,6 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
             }
             have = true;
             if (INSTR) st.phase[release ? PH_WL_REMOVE : PH_STACK] += clock64() - t0;
-            if (VCG_TIMELINE && first_pop) {
-                first_pop = false;
-                if (lane == 0) my_stats->t_first = globaltimer();
-            }
         }
 
         // Every worker polling the one control line at every node queues thousands of reads on
@@ -1940,6 +1971,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 }
                 if (worker == (MULTI ? 1u : 0u) && a.mailbox) poll_mailbox(a.mailbox, a.pvc, ctl);
                 fold_stats(my_stats, st);
+                if (kCntSmem) fold_cw();
             }
             reset_deltas(st);
             if (__shfl_sync(FULL, stop, 0)) break;
@@ -1983,11 +2015,12 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
     if (lane == 0) {
         if (st.nodes) atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes);
         fold_stats(my_stats, st);
-        my_stats->high_water = st.high_water;
+        if (kCntSmem) fold_cw();
+        my_stats->high_water = kCntSmem ? cw[CW_HIGH] : st.high_water;
         my_stats->active = clock64() - c_start;
         my_stats->t_begin = t0s[0];
         my_stats->t_end = globaltimer();
-        my_stats->max_queue = st.max_queue;
+        my_stats->max_queue = kCntSmem ? cw[CW_MAXQ] : st.max_queue;
 #pragma unroll
         for (int p = 0; p < 10; ++p) my_stats->phase[p] = INSTR ? st.phase[p] : 0ull;
     }
