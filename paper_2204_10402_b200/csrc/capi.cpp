@@ -371,8 +371,9 @@ namespace {
 // Debug option (VCG_DEBUG_CERTIFY): re-prove a parallel MVC optimum by PVC(s - 1). The PVC search
 // has no bound dynamics (its tree and node count are the reference's exactly), so a "no" proves
 // the size s found optimal and a "yes" improves the certificate and repeats. The parallel MVC
-// search is exact on its own (the dense engine re-reduces a node when a poll lowers the bound
-// before the edge-count prune; see settle() in dense_kernels.cuh), so this is off by default;
+// search is exact on its own (the dense engine's edge-count prune uses the bound its reduction
+// reached fixpoint under, even when a poll lowered the bound since; see settle() in
+// dense_kernels.cuh), so this is off by default;
 // it exists to cross-check that claim. Its nodes and device time are reported separately
 // (certify_nodes / certify_ms), and it only spends what is left of the caller's time and node
 // limits.

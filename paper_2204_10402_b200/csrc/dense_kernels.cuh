@@ -312,6 +312,10 @@ constexpr uint32_t kPoll = VCG_POLL_EVERY;
 #ifndef VCG_FROM_WIDE_BALLOT
 #define VCG_FROM_WIDE_BALLOT 1  // compact conversion: rows by ballots over slots (see from_wide)
 #endif
+#ifndef VCG_RELAXED_FREE
+#define VCG_RELAXED_FREE 0  // A/B only: the slot-free signal as a relaxed store (the slot's values
+                            // are consumed before it, but the PTX model does not order them)
+#endif
 #ifndef VCG_CNT_SMEM
 #define VCG_CNT_SMEM 1  // (W >= 16) per-branch counters in the warp's shared slot, not registers
 #endif
@@ -1475,7 +1479,9 @@ __device__ __noinline__ void exchange_helper(Ctl* ctl, const PeerRef* peers, uin
             pos = atomicAdd(&ctl->head, 1ull);
 #pragma unroll 1
             for (uint32_t spin = 0;; ++spin) {
-                if (ld_acquire_sys_u64(seq + (pos & ring_mask)) == pos + 1) {
+                // (relaxed polls — an acquire invalidates the SM's L1, the search warps' spill
+                // and local-memory lines included; every lane acquires once it has matched)
+                if (ld_relaxed_sys_u64(seq + (pos & ring_mask)) == pos + 1) {
                     got = 1;
                     break;
                 }
@@ -1868,7 +1874,10 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 for (uint32_t spin = 0;; ++spin) {
                     int o = 0;
                     if (lane == 0) {
-                        if ((multi && !VCG_TEST_GPU_ACQ ? ld_acquire_sys_u64(release) : ld_acquire_u64(release)) == pos + 1) o = 1;
+                        // relaxed polls: an acquire load invalidates the SM's whole L1 (CCTL.IVALL),
+                        // the working warps' local-memory lines included, at every spin of every
+                        // idle warp; the publication is acquired once, below, after the match
+                        if ((multi && !VCG_TEST_GPU_ACQ ? ld_relaxed_sys_u64(release) : ld_relaxed_u64(release)) == pos + 1) o = 1;
                         else if ((spin & 7) == 7) {
                             if (ld_volatile_v4(ctl).y) o = 2;
                             else if ((ld_relaxed_u64(&ctl->work) >> 32) == 0 &&
@@ -1931,7 +1940,10 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 // warp barrier (cumulativity): no full fence needed
                 __syncwarp();
                 if (lane == 0) {
-                    st_release_u64(release, pos + a.ring_mask + 1);  // free for the next lap
+                    if (VCG_RELAXED_FREE && !multi)  // (A/B only, see VCG_RELAXED_FREE)
+                        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(release), "l"(pos + a.ring_mask + 1) : "memory");
+                    else
+                        st_release_u64(release, pos + a.ring_mask + 1);  // free for the next lap
                     atomicAdd(&ctl->work, ~0ull);                     // size - 1
                 }
             }

@@ -492,8 +492,9 @@ def _fuzz_graph(name):
 def test_parallel_mvc_is_exact_without_certificate(oracle, name):
     """Regression (tools/fuzz_parity.py, round 1): on these graphs the parallel MVC search once
     stopped one above the optimum — the edge-count prune used a bound lowered by a poll AFTER
-    the node was reduced under the older one. With the node re-reduced under the new bound
-    (settle(), dense_kernels.cuh) every strategy, engine and the multi-shard path are exact on
+    the node was reduced under the older one. With the edge-count prune under the bound the
+    reduction reached fixpoint under (settle(), dense_kernels.cuh) every strategy, engine and the
+    multi-shard path are exact on
     their own; the racing schedule differs run to run, so each runs several times."""
     from oracle.oracle import CSR
     from paper_2204_10402_b200.shards import solve_sharded
