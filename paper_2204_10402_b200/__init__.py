@@ -214,6 +214,7 @@ def _solve(graph, mode, k, strategy, workers, capacity, threshold_fraction, dept
         _lib.vcg_result_free(C.byref(r))
     del keep
     if raw:
+        out.pop("_worker_nodes_np", None)
         return out
     return make_report(graph, mode, k, strategy, workers if workers else out["num_workers"],
                        capacity, threshold_fraction, depth, out)
@@ -285,6 +286,13 @@ def _array(ptr, count):
     return np.ctypeslib.as_array(ptr, shape=(count,)).tolist()
 
 
+def _array_np(ptr, count):
+    """A copy of a library-owned C array as a numpy array (valid after vcg_result_free)."""
+    if count == 0 or not ptr:
+        return np.zeros(0, dtype=np.uint64)
+    return np.ctypeslib.as_array(ptr, shape=(count,)).copy()
+
+
 def _result_dict(r):
     nw = r.num_workers
     return dict(
@@ -293,6 +301,9 @@ def _result_dict(r):
         cover=_array(r.cover, r.cover_len),
         cover_from_search=bool(r.cover_from_search), num_workers=nw,
         worker_nodes=_array(r.worker_nodes, nw),
+        # (the same counts as an array: the report's load ratios without a list -> array pass
+        # over thousands of device workers on the host's critical path between solves)
+        _worker_nodes_np=_array_np(r.worker_nodes, nw),
         worker_stack_high_water=_array(r.worker_stack_high_water, nw),
         nodes_total=int(r.nodes_total),
         worklist=dict(added=int(r.wl_added), removed=int(r.wl_removed),

@@ -35,8 +35,8 @@ def collect_metrics(worker_nodes, phase_cycles, active_cycles):
 
 
 def make_report(graph, mode, k, strategy, workers, capacity, threshold_fraction, depth, res):
-    ratios, shares = collect_metrics(res["worker_nodes"], res["phase_cycles"],
-                                     res["active_cycles"])
+    ratios, shares = collect_metrics(res.get("_worker_nodes_np", res["worker_nodes"]),
+                                     res["phase_cycles"], res["active_cycles"])
     rep = {
         "n": graph.num_vertices,
         "m": graph.num_edges,

@@ -80,7 +80,9 @@ class Shard:
         r = _n.Result()
         _n.check(_lib.vcg_session_wait(self._h, C.byref(r)))
         try:
-            return _result_dict(r)
+            out = _result_dict(r)
+            out.pop("_worker_nodes_np", None)
+            return out
         finally:
             _lib.vcg_result_free(C.byref(r))
 
