@@ -351,6 +351,26 @@ __device__ __forceinline__ uint32_t dense_degree_base(uint32_t wib) {
 // renumbered in id order into slots, their induced adjacency rows in a per-warp FRAME bitmap in
 // shared memory, degrees in registers. Every primitive is the wide one on a W-word bitmap, so
 // the same reduce_node runs on it and, slots keeping the id order, acts on the same vertices.
+// (VCG_WIDE_COLD, A/B only) the wide layout's record load, child pass and child store out of
+// line, to take their large bodies out of the compact hot loop's instruction footprint.
+// Measured: C5 8.9 -> 10.0 ms, C5-scale -5% (the calls' register saves and restores add
+// spills at the 72-register budget): off.
+#ifndef VCG_WIDE_COLD
+#define VCG_WIDE_COLD 0
+#endif
+template <class N>
+__device__ __noinline__ void wide_load_cold(N& x, const unsigned char* rec) { x.load_body(rec); }
+template <class N>
+__device__ __noinline__ bool wide_child_pass_cold(const N& x, uint32_t xl, uint32_t xcnt, int B,
+                                                  uint32_t& keep, uint32_t dmax) {
+    return x.template child_pass<true>(xl, xcnt, B, keep, dmax);
+}
+template <class N>
+__device__ __noinline__ void wide_store_child_cold(const N& x, uint32_t keepm, uint32_t xcnt,
+                                                   unsigned char* rec) {
+    x.store_child(keepm, xcnt, rec);
+}
+
 template <int W, bool INSTR, int WG = 0>
 struct WarpNode {
     static constexpr bool kInstr = INSTR;
@@ -532,10 +552,14 @@ struct WarpNode {
     }
     template <bool TEST>
     __device__ __forceinline__ bool child_pass(Child& c, int B, uint32_t dmax) const {
-        return child_pass<TEST>(c.xl, c.xcnt, B, c.keepm, dmax);
+        if constexpr (!IND && VCG_WIDE_COLD && TEST)
+            return wide_child_pass_cold(*this, c.xl, c.xcnt, B, c.keepm, dmax);
+        else
+            return child_pass<TEST>(c.xl, c.xcnt, B, c.keepm, dmax);
     }
     __device__ __forceinline__ void child_store(const Child& c, unsigned char* rec) const {
-        store_child(c.keepm, c.xcnt, rec);
+        if constexpr (!IND && VCG_WIDE_COLD) wide_store_child_cold(*this, c.keepm, c.xcnt, rec);
+        else store_child(c.keepm, c.xcnt, rec);
     }
     template <int WW>
     __device__ __forceinline__ uint32_t cover_word(uint32_t* sb) const {
@@ -663,10 +687,11 @@ struct WarpNode {
     }
     // Loads a record through L2 (it may come from another SM's worklist donation).
     __device__ __forceinline__ void load(const unsigned char* rec) {
-        if constexpr (IND) {
-            load_mid(rec);
-            return;
-        }
+        if constexpr (IND) load_mid(rec);
+        else if constexpr (VCG_WIDE_COLD) wide_load_cold(*this, rec);
+        else load_body(rec);
+    }
+    __device__ __forceinline__ void load_body(const unsigned char* rec) {
         uint32_t packed[W / 2];
         const unsigned char* p = rec + 16 + lane * (2 * W);
         if constexpr (W == 4) {
