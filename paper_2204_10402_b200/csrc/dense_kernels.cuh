@@ -50,15 +50,19 @@ struct Ctl {
     // line 0: read by every worker once per node (one vector load + one scalar load)
     uint32_t best;    // MVC bound (atomicMin); PVC: k
     uint32_t cancel;  // 1 = stop: PVC found, timeout, budget, host request
-    uint32_t found;   // PVC: a cover of size <= k was recorded
-    uint32_t pad0;
 #if !VCG_SPLIT_WORK
     // (pending << 32) | size: pending = queued items + active workers (termination at 0);
-    // size = queued items + in-flight enqueue reservations (threshold gate, capacity)
+    // size = queued items + in-flight enqueue reservations (threshold gate, capacity).
+    // {best, cancel, work} are the first 16 bytes: the dense workers' poll copies them to
+    // shared memory with one cp.async.
     unsigned long long work;
+    uint32_t found;   // PVC: a cover of size <= k was recorded
+    uint32_t pad0;
     unsigned long long pad1;
     uint32_t pad2[24];
 #else
+    uint32_t found;
+    uint32_t pad0;
     uint32_t pad2[28];
     // line 0b: the packed worklist word on its own line (its atomics do not contend with the
     // reads of the bound / cancel words)
@@ -315,6 +319,11 @@ constexpr uint32_t kPoll = VCG_POLL_EVERY;
 #ifndef VCG_RELAXED_FREE
 #define VCG_RELAXED_FREE 0  // A/B only: the slot-free signal as a relaxed store (the slot's values
                             // are consumed before it, but the PTX model does not order them)
+#endif
+#ifndef VCG_POLL_SMEM
+#define VCG_POLL_SMEM 0  // (W >= 16) the control-line poll lands in shared memory by cp.async:
+                         // no registers across the reduction (C5 kernel spills 36 -> 4 B) but
+                         // measured C5 equal, C5-scale 2% slower than register polls: off
 #endif
 #ifndef VCG_CNT_SMEM
 #define VCG_CNT_SMEM 1  // (W >= 16) per-branch counters in the warp's shared slot, not registers
@@ -1626,19 +1635,25 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         reinterpret_cast<uint32_t*>(dense_smem) + (W / 4) * (32 * W) * 4 + wib * W);
     // (W >= 16: words 4..7 of the slot hold the mid layout's current frame tag and tag counter)
     static_assert(MW == 0 || (W >= 16 && (MW == 4 || MW == 8)), "mid layout width");
-    // (W >= 16, VCG_CNT_SMEM: words 8..12 hold lane 0's per-branch counters — branches,
-    // children stored, donations, stack high water, queue maximum — instead of five registers
+    // (W >= 16, VCG_CNT_SMEM: words 8..10 hold lane 0's per-branch counters — branches,
+    // children stored and donations packed 10 bits each (deltas between flushes, at most
+    // flush_every <= 64 each), stack high water, queue maximum — instead of five registers
     // live across the node loop: the hot loop's register budget sets the occupancy, and the
-    // counters change at most once per branch)
+    // counters change at most once per branch. Words 12..15: the poll's copy of the control
+    // line's first 16 bytes {best, cancel, work}, landed by cp.async — no registers held from
+    // the poll's issue to its use after the reduction.)
     constexpr bool kCntSmem = VCG_CNT_SMEM && W >= 16;
+    constexpr bool kPollSmem = VCG_POLL_SMEM && W >= 16 && !VCG_SPLIT_WORK;
     uint32_t* const cw = reinterpret_cast<uint32_t*>(t0s) + 8;
-    enum { CW_MAXDEG = 0, CW_CHILDREN, CW_DONATED, CW_HIGH, CW_MAXQ };
+    enum { CW_PACKED = 0, CW_HIGH = 1, CW_MAXQ = 2 };
+    constexpr uint32_t CWP_MAXDEG = 1u, CWP_CHILDREN = 1u << 10, CWP_DONATED = 1u << 20;
+    uint32_t* const pw = reinterpret_cast<uint32_t*>(t0s) + 12;
     if (lane == 0) {
         t0s[0] = globaltimer();
         t0s[1] = (unsigned long long)clock64();
         if (kCntSmem)
 #pragma unroll
-            for (int i = 0; i < 5; ++i) cw[i] = 0;
+            for (int i = 0; i < 3; ++i) cw[i] = 0;
         if (MW) {
             t0s[2] = 0;  // no frame
             t0s[3] = ((unsigned long long)a.rank << 56) | ((unsigned long long)(worker + 1) << 36);
@@ -1682,10 +1697,11 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
     Ctl* ctl = a.ctl;
 #define my_stats (a.stats + worker)
     auto fold_cw = [&]() {  // (lane 0)
-        my_stats->maxdeg += cw[CW_MAXDEG];
-        my_stats->children += cw[CW_CHILDREN];
-        my_stats->donated += cw[CW_DONATED];
-        cw[CW_MAXDEG] = cw[CW_CHILDREN] = cw[CW_DONATED] = 0;
+        const uint32_t pk = cw[CW_PACKED];
+        my_stats->maxdeg += pk & 1023u;
+        my_stats->children += (pk >> 10) & 1023u;
+        my_stats->donated += pk >> 20;
+        cw[CW_PACKED] = 0;
     };
 #define my_stack (a.stacks + (unsigned long long)worker * a.stack_bound * a.entry_bytes)
     // The local stack is a ring [base, base + sp) so its oldest entry can be donated.
@@ -1744,12 +1760,24 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         const int Br = B;
         reduce_under_B(n);
         if (VCG_UNLIKELY(poll)) {
-            if (__shfl_sync(FULL, h.y, 0)) return ACT_BREAK;
+            uint32_t pb, pc, pq;  // the polled {best, cancel, size}
+            if constexpr (kPollSmem) {
+                if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+                pb = pw[0];
+                pc = pw[1];
+                pq = pw[2];
+            } else {
+                pb = __shfl_sync(FULL, h.x, 0);
+                pc = __shfl_sync(FULL, h.y, 0);
+                pq = __shfl_sync(FULL, hw, 0);
+            }
+            if (pc) return ACT_BREAK;
             if (!a.pvc) {
-                best = min(best, __shfl_sync(FULL, h.x, 0));
+                best = min(best, pb);
                 B = bound_of(0, 0, best);
             }
-            qsize = __shfl_sync(FULL, hw, 0);
+            qsize = pq;
         }
         const bool prune = n.doom || prune_at(Br, n.cc, n.edges) || (int)n.cc > B;
         st.dooms += n.doom;
@@ -1772,7 +1800,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         long long tm = INSTR ? clock64() : 0;
         uint32_t dmax;
         const uint32_t v = n.argmax(dmax);
-        if (kCntSmem) { if (lane == 0) ++cw[CW_MAXDEG]; } else ++st.maxdeg;
+        if (kCntSmem) { if (lane == 0) cw[CW_PACKED] += CWP_MAXDEG; } else ++st.maxdeg;
         if (INSTR) st.phase[PH_MAXDEG] += clock64() - tm;
         long long tb = INSTR ? clock64() : 0;
         // StackOnly replay of the root path: branch bit `replay` of the sub-tree id picks the
@@ -1823,7 +1851,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 } else {
                     child = dst;
                 }
-                if (kCntSmem) { if (lane == 0) ++cw[CW_DONATED]; } else ++st.donated;
+                if (kCntSmem) { if (lane == 0) cw[CW_PACKED] += CWP_DONATED; } else ++st.donated;
             }
         }
         if (build && (!dead || seq_mode_)) {
@@ -1837,7 +1865,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
                 if (lane == 0) *reinterpret_cast<uint4*>(child) = make_uint4(DEAD_NODE, 0u, 0u, 0u);
             } else {
                 n.child_store(c, child);
-                if (kCntSmem) { if (lane == 0) ++cw[CW_CHILDREN]; } else ++st.children;
+                if (kCntSmem) { if (lane == 0) cw[CW_PACKED] += CWP_CHILDREN; } else ++st.children;
             }
         }
         if (publish) {
@@ -1983,8 +2011,16 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
         // issued here and consumed after the reduction.
         poll = (++polls & (kPollK - 1)) == 0;
         if (poll && lane == 0) {
-            h = ld_volatile_v2(ctl);
-            hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
+            if constexpr (kPollSmem) {
+                // L2 -> shared memory (.cg: not through L1, so the line is as fresh as a relaxed
+                // load's; a stale bound only prunes less, a stale size only steers donation)
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pw);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;"
+                             ::"r"(dst), "l"(ctl) : "memory");
+            } else {
+                h = ld_volatile_v2(ctl);
+                hw = ld_relaxed_u32(&ctl->work);  // (low word: size)
+            }
         }
 
         // visit_and_check_limits (scheduler.cpp:63-74), batched per flush_every visits
@@ -2050,6 +2086,7 @@ __global__ void __launch_bounds__(32 * BW, (BW != 8 ? 1 : (W <= 8 ? VCG_MINB8 : 
     }
 
     if (lane == 0) {
+        if (kPollSmem) asm volatile("cp.async.wait_all;" ::: "memory");  // (a poll left in flight)
         if (st.nodes) atomicAdd(&ctl->nodes_total, (unsigned long long)st.nodes);
         fold_stats(my_stats, st);
         if (kCntSmem) fold_cw();
