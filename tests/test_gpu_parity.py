@@ -132,6 +132,23 @@ def test_c5_pvc_no_instance_node_count(config_golden):
     check_cover(g, y)
 
 
+def test_c5_engine_counters_are_schedule_independent():
+    """On a PVC no-instance every tree node is visited once under the same bound k, so the
+    rule work per node is fixed: rule rounds, branches (max-degree passes), stored children,
+    removals per rule and prunes (dooms, dead children included) do not depend on the schedule.
+    Guards the counters' bookkeeping (per-branch counters packed in shared memory, flushed per
+    64 visits) against the values the round-1 kernels reported for the same tree."""
+    g = load_config("c5")
+    want = dict(rounds=14332419, maxdeg_passes=10730684, children=2403990,
+                removals_deg1=1379027, removals_deg2=2015806, removals_high=6824878,
+                doomed=9135007)
+    for kw in (dict(), dict(block_warps=8)):
+        r = vc.solve_pvc(g, 482, strategy="gpu", **kw)
+        assert r["nodes_total"] == 21461369
+        assert {k: r[k] for k in want} == want
+        assert 0 < r["donated"] <= r["maxdeg_passes"]  # (at most one donation per branch)
+
+
 def test_budget_and_timeout_status():
     g = load_config("c1")
     r = vc.solve_mvc(g, strategy="gpu", node_budget=1000)
